@@ -1,0 +1,295 @@
+"""Benchmark: DoFs/s per matrix-free Laplace apply (3D Q_k, FP64) on B200.
+
+A "step" is one mf_apply -- the whole per-apply hot path of SURVEY.md §8(a)
+(a3 gather .. a7 scatter + Dirichlet identity, and the a8 halo exchange when
+N > 1) -- over one synthetic input vector.  Setup rows (a1 tables, a2 geometry,
+a9 diagonal) run once before timing; a10 (the solver) is measured by
+``--solve``.  Workload at N = 1: BASELINE.json configs[2], Q4 on a 64^3 unit
+cube, affine, c = 1, Dirichlet on all faces (16,974,593 DoFs); src + dst =
+272 MB > 126 MB L2, so every timed apply streams from HBM.  N > 1 (torchrun):
+weak scaling, rank r holds 64 z-layers of a 64 x 64 x (64 N) brick, halo
+planes exchanged with NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mf|reference]
+                  [--config cfg3|cfg4|cfg2|cfg5q4|cfg5q6] [--solve]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n_cells per rank (z multiplied by N), degree, geometry, coeff, description)
+    "cfg3": ((64, 64, 64), 4, "cartesian", 1.0, "3D Laplace Q4 on 64^3 cube (~17M DoFs), affine, c=1"),
+    "cfg4": ((64, 64, 64), 3, "sine", "variable", "3D variable-coefficient Laplace Q3 on deformed 64^3 cube, stored metric"),
+    "cfg2": ((16, 16, 16), 2, "cartesian", 1.0, "3D Laplace Q2 on 16^3 affine cube"),
+    "cfg5q4": ((256, 256, 256), 4, "cartesian", 1.0, "3D Laplace Q4 on 256^3 cube (~1.08B DoFs)"),
+    "cfg5q6": ((256, 256, 256), 6, "cartesian", 1.0, "3D Laplace Q6 on 256^3 cube (~3.6B DoFs)"),
+}
+METRIC = "DoFs/s per matrix-free Laplace apply (3D Q_k FP64)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
+    def sample(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline_sample(degree, geometry, coeff, seconds=10.0, cells=16):
+    """The oracle as it stands (C/OpenMP CSR assembly + SpMV) on a bounded
+    sample of the workload: the same element type and geometry on a cells^3
+    sub-brick; SpMV repeated for ~`seconds`.  Returns DoFs/s and a description."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    p = oracle.problem(dim=3, n_cells=(cells,) * 3, degree=degree, geom=1 if geometry == "sine" else 0,
+                       coeff_kind=1 if coeff == "variable" else 0, coeff_value=1.0 if coeff == "variable" else coeff)
+    t0 = time.perf_counter()
+    A = oracle.CSR(p)
+    t_asm = time.perf_counter() - t0
+    x = synth.vector(A.n, 0)
+    y = np.empty_like(x)
+    A.matvec(x, y)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        A.matvec(x, y)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return A.n * reps / el, A.n, reps, el, t_asm, oracle.num_threads()
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle timed as it stands on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    nc, k, geom, coeff, desc = CONFIGS[cfg]
+    import numpy as np
+
+    import oracle
+    import synth
+
+    cells = 16
+    p = oracle.problem(dim=3, n_cells=(cells,) * 3, degree=k, geom=1 if geom == "sine" else 0,
+                       coeff_kind=1 if coeff == "variable" else 0, coeff_value=1.0 if coeff == "variable" else coeff)
+    A = oracle.CSR(p)
+    x = synth.vector(A.n, 0)
+    y = np.empty_like(x)
+    for _ in range(args.warmup):
+        A.matvec(x, y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        A.matvec(x, y)
+    el = time.perf_counter() - t0
+    v = A.n * args.steps / el
+    sample = f"oracle CSR SpMV (assembled by full Gauss quadrature) of the same Q{k} operator on a {cells}^3 sub-brick ({A.n} DoFs), one SpMV per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "DoFs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "DoFs/s", "cores": oracle.num_threads(), "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "DoFs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="mf", choices=["mf", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--variant", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solve", action="store_true", help="also time one Chebyshev(6)-PCG solve")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_1910_13247_b200 import Operator
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    nc, k, geom, coeff, desc = CONFIGS[args.config]
+    nc = (nc[0], nc[1], nc[2] * world)
+    op = Operator(nc, k, geometry=geom, coeff=coeff, group=group, device=local)
+    op.set_variant(args.variant)
+    n = op.n_local
+    src = torch.from_numpy(synth.uniform(op.first_global, n, 0)).cuda()
+    dst = torch.empty_like(src)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        op.apply(src, dst)
+    barrier()
+    info0 = op.info()
+    clocks = ClockSampler(local)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    op.kernel_timing(True)
+    with clocks:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            op.apply(src, dst)
+        stop.record(stream)
+        barrier()
+    op.kernel_timing(False)
+    info1 = op.info()
+    ms = start.elapsed_time(stop)
+    kern_ms, kern_n = op.kernel_time()
+    t = torch.tensor([ms, kern_ms / max(kern_n, 1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, kern_avg_ms = t[0].item(), t[1].item()
+    ms_per_step = ms_max / args.steps
+    value = op.n_global * args.steps / (ms_max * 1e-3)
+    launches = (info1["kernel_launches"] - info0["kernel_launches"])
+
+    # end to end through the public C ABI with pinned host buffers (H2D + apply + D2H each step)
+    hs = torch.from_numpy(synth.uniform(op.first_global, n, 0)).pin_memory()
+    hd = torch.empty_like(hs).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    op.apply_host_ptr(hs.data_ptr(), hd.data_ptr())
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        op.apply_host_ptr(hs.data_ptr(), hd.data_ptr())
+    barrier()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_val = op.n_global * e2e_steps / e2e_s.item()
+    # parity spot check of the timed output (cheap invariant: identity rows)
+    ok = bool(torch.equal(dst[:op.mesh.n_cells[0] * k + 1], src[:op.mesh.n_cells[0] * k + 1])) if rank == 0 else True
+
+    solve = None
+    if args.solve:
+        b = torch.ones(n, dtype=torch.float64, device="cuda")
+        barrier()
+        t0 = time.perf_counter()
+        x, res = op.cg_solve(b, rel_tol=1e-10)
+        barrier()
+        solve = {"iterations": res.iterations, "seconds": time.perf_counter() - t0, "lambda_max": res.lambda_max}
+
+    if rank == 0:
+        peak, peak_kind = load_peaks()
+        bytes_per_launch = info1["bytes_algorithmic"]
+        achieved = bytes_per_launch / (kern_avg_ms * 1e-3) / 1e9
+        out = {
+            "metric": METRIC, "value": value, "unit": "DoFs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "config": args.config, "n_cells": list(nc), "degree": k,
+                       "n_dofs": op.n_global, "geometry": geom, "coeff": coeff, "parallelism": f"zslab{world}",
+                       "apply_variant": info1["apply_variant"],
+                       "l2": f"inputs larger than L2: src+dst {16 * n / 1e6:.0f} MB per GPU > 126 MB"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_launch": bytes_per_launch, "kernel_ms": kern_avg_ms,
+                         "kernel_share_of_step": kern_avg_ms / ms_per_step},
+            "e2e": {"value": e2e_val, "unit": "DoFs/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "steps": e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "identity_rows_exact": ok,
+        }
+        if solve:
+            out["solve"] = solve
+        if not args.no_cpu_baseline and world == 1:
+            v, nd, reps, el, t_asm, cores = cpu_baseline_sample(k, geom, coeff)
+            out["cpu_baseline"] = {"value": v, "unit": "DoFs/s", "cores": cores, "kind": "oracle",
+                                   "sample": f"oracle CSR SpMV of the same Q{k} operator on a 16^3 sub-brick ({nd} DoFs), {reps} SpMVs in {el:.1f} s (assembly {t_asm:.1f} s not timed)"}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

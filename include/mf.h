@@ -1,0 +1,172 @@
+/* mf.h -- C ABI of the B200-native matrix-free Laplace library (libmf_b200.so).
+ *
+ * The library evaluates v = A u for the finite-element discretisation of the
+ * Laplacian of PAPER.md Eq. (1) (§2.4: a(u,v) = (grad u, grad v)_Omega,
+ * with a constant or variable coefficient c(x)) without ever building a matrix
+ * (§3.6: "a global sparse matrix is never built and linear systems
+ * are only solved by the action of the underlying linear operator on a vector
+ * via the integrals in the weak form"), by sum factorisation over the
+ * tensor-product Q_k shape functions (§3.6) on a structured brick of
+ * hexahedra (quadrilaterals in 2D), affine or curved (isoparametric degree k).
+ * Around it sit the operator diagonal and a Chebyshev(6)-Jacobi preconditioned
+ * CG (§6.1 "Chebyshev smoothing of degree 6").
+ *
+ * Discretisation: Gauss-Legendre quadrature with k+1
+ * points per direction (R1); Gauss-Lobatto support points, x-fastest
+ * lexicographic global numbering g = (gz*Ny + gy)*Nx + gx with N_e = k*n_e + 1
+ * (R2); homogeneous Dirichlet rows/columns replaced by the identity, dst_g = src_g
+ * (R3); curved geometry Phi(x) = x + eps (hi-lo) prod_d sin(pi (x_d-lo_d)/(hi_d-lo_d))
+ * (R4); variable coefficient c(x) = 1/(0.05 + 2|x|^2) (R5).
+ *
+ * Conventions
+ *  - Every vector is caller-owned, contiguous FP64.  mf_apply / mf_diagonal /
+ *    mf_chebyshev take DEVICE pointers (e.g. torch.Tensor.data_ptr()) and are
+ *    asynchronous on the op's stream; mf_apply_host takes HOST pointers and
+ *    blocks.  The library never frees or retains caller pointers.
+ *  - With world_size > 1 the brick is cut into z-slabs of whole cell layers;
+ *    rank r holds the contiguous global range [first_global, first_global +
+ *    n_local): its DoF planes plus a duplicate of the shared upper plane
+ *    (owned, for dot products, by the upper rank; the first n_owned entries are
+ *    this rank's owned DoFs).  Every call is then collective (same order and
+ *    arguments on every rank, as in NCCL).
+ *  - Errors: negative mf_status, message from mf_last_error() (thread-local).
+ *    An op is not thread-safe.
+ */
+#ifndef MF_B200_H
+#define MF_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MF_OK = 0,
+  MF_ERR_ARGUMENT = -1,       /* bad descriptor: dim, degree 1..8, n_cells < 1, lower >= upper, NULL (S:148 BadDomain) */
+  MF_ERR_LENGTH = -2,         /* vector length != n_local (S:566 LengthMismatch) */
+  MF_ERR_SINGULAR = -3,       /* det J <= 0 at a quadrature point (S:332 SingularTensor) */
+  MF_ERR_MAX_ITERATIONS = -4, /* CG did not converge within max_iter */
+  MF_ERR_BREAKDOWN = -5,      /* p.Ap <= 0 or r.z <= 0 in CG / eigenvalue estimate */
+  MF_ERR_CUDA = -6,
+  MF_ERR_NCCL = -7,
+  MF_ERR_OUT_OF_MEMORY = -8
+} mf_status;
+
+enum { MF_GEOM_CARTESIAN = 0, MF_GEOM_SINE = 1 };
+enum { MF_COEFF_CONSTANT = 0, MF_COEFF_VARIABLE = 1 };
+
+/* Structured brick [lower, upper] with n_cells[e] cells per direction e < dim. */
+typedef struct {
+  int32_t dim;              /* 2 or 3 */
+  int64_t n_cells[3];       /* >= 1 for e < dim; ignored otherwise */
+  double lower[3], upper[3];
+  int32_t geometry;         /* MF_GEOM_CARTESIAN or MF_GEOM_SINE (R4, isoparametric degree k) */
+  double deform_eps;        /* eps of R4 (0.1 in BASELINE cfg 4) */
+  uint32_t dirichlet_faces; /* bit f for face f = x-,x+,y-,y+,z-,z+ (S:147); 0 = pure Neumann */
+} mf_mesh;
+
+typedef struct {
+  int32_t kind;  /* MF_COEFF_CONSTANT (c = value) or MF_COEFF_VARIABLE (c(x) of R5) */
+  double value;
+} mf_coeff;
+
+/* Multi-GPU placement; pass NULL to mf_create for one GPU on the current device. */
+typedef struct {
+  int32_t rank, world_size;
+  const uint8_t *nccl_unique_id; /* 128 bytes from mf_nccl_unique_id() on rank 0; NULL if world_size == 1 */
+  int32_t device;                /* CUDA device ordinal for this rank */
+} mf_dist;
+
+typedef struct mf_op mf_op; /* opaque, owned by the library */
+
+/* Build the operator: 1D tables, geometry (metric precompute for MF_GEOM_SINE,
+ * MF_ERR_SINGULAR if det J <= 0), Dirichlet plan, z-slab partition and NCCL
+ * communicator.  Collective when world_size > 1. */
+mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff,
+                    const mf_dist *dist, mf_op **out);
+void mf_destroy(mf_op *op);
+const char *mf_last_error(void);
+
+/* NCCL unique id (128 bytes) for mf_dist, created on rank 0 and broadcast by the caller. */
+mf_status mf_nccl_unique_id(uint8_t *out128);
+
+/* Local / global sizes (see Conventions). */
+mf_status mf_sizes(const mf_op *op, int64_t *n_local, int64_t *first_global,
+                   int64_t *n_global, int64_t *n_owned);
+
+/* cudaStream_t on which every asynchronous call is enqueued (default: the
+ * legacy default stream of the op's device). */
+mf_status mf_set_stream(mf_op *op, void *cuda_stream);
+
+/* dst = A src (§8(a) a3-a8: gather, sum factorisation to the Gauss points,
+ * quadrature-point operation, transposed sweeps, scatter-add, Dirichlet
+ * identity, halo exchange for world_size > 1).  src and dst are distinct
+ * device buffers of n_local doubles; dst is overwritten.  Asynchronous. */
+mf_status mf_apply(mf_op *op, const double *src, int64_t n_src, double *dst, int64_t n_dst);
+
+/* The same with HOST buffers: H2D copy of src, apply, D2H copy of dst; blocks. */
+mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_src, double *dst_host,
+                        int64_t n_dst);
+
+/* diag = diagonal of A (§8(a) a9), 1 on constrained DoFs.  Asynchronous. */
+mf_status mf_diagonal(mf_op *op, double *diag, int64_t n);
+
+/* Largest Ritz value of D^{-1}A from `steps` Jacobi-PCG steps started from the
+ * splitmix64 vector of the global DoF index (seed 0, zero on constrained DoFs),
+ * without the safety factor (R8).  Blocks. */
+mf_status mf_estimate_lambda_max(mf_op *op, int32_t steps, double *lambda_out);
+
+/* z = Chebyshev(degree) approximation of A^{-1} r for D^{-1}A on
+ * [lambda/smoothing_range, lambda], started from zero (R6, R7).
+ * Device buffers of n_local doubles.  Asynchronous. */
+mf_status mf_chebyshev(mf_op *op, const double *r, double *z, int64_t n, double lambda,
+                       int32_t degree, double smoothing_range);
+
+typedef struct {
+  double rel_tol;        /* stop when ||r||_2 <= rel_tol ||b||_2 (recursive residual, R9) */
+  int32_t max_iter;      /* applications of A, e.g. 10000 */
+  int32_t cheb_degree;   /* 6; 0 selects plain Jacobi-PCG */
+  double cheb_range;     /* 20 */
+  double cheb_safety;    /* 1.2 */
+  int32_t eig_cg_steps;  /* 12 */
+} mf_cg_params;
+
+typedef struct {
+  int32_t iterations;        /* applications of A in the CG loop (not counting the eigenvalue estimate / preconditioner) */
+  double final_rel_residual; /* ||r_N|| / ||b|| */
+  double lambda_max;         /* safety * Ritz estimate used by the Chebyshev preconditioner */
+} mf_cg_result;
+
+/* Solve A x = b from x0 = 0 with Chebyshev(cheb_degree)-Jacobi PCG (§8(a) a10,
+ * S:500-508).  b, x: device buffers of n_local doubles.  Optional residual
+ * history: if history != NULL it receives ||r_j|| after each apply (up to
+ * history_cap entries).  Blocks (the host reads 2-3 scalars per iteration). */
+mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t n, const mf_cg_params *params,
+                      mf_cg_result *result, double *history, int32_t history_cap);
+
+/* Introspection for tests and the benchmark. */
+typedef struct {
+  int32_t dim, degree, geometry, coeff_kind;
+  int32_t apply_variant;      /* kernel family chosen for mf_apply */
+  int64_t n_cells_local;
+  int64_t kernel_launches;    /* cumulative count of this library's kernel launches on this op */
+  int64_t bytes_algorithmic;  /* algorithmic HBM bytes of one apply: 16 B/DoF + stored geometry */
+  double flops_algorithmic;   /* FP64 flops of one apply for the chosen variant */
+} mf_info;
+mf_status mf_get_info(const mf_op *op, mf_info *info);
+
+/* Force a kernel family for mf_apply (0 = automatic).  Unknown or unsupported
+ * choices return MF_ERR_ARGUMENT. */
+mf_status mf_set_apply_variant(mf_op *op, int32_t variant);
+
+/* Live timing of the dominant cell kernel of mf_apply with CUDA events recorded
+ * on the op's stream around each launch (enable != 0 starts a new window).
+ * mf_kernel_timing synchronises those events and returns the summed
+ * milliseconds and the number of timed launches since the window started. */
+mf_status mf_set_kernel_timing(mf_op *op, int32_t enable);
+mf_status mf_kernel_timing(mf_op *op, double *ms_total, int64_t *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MF_B200_H */

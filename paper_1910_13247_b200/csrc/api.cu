@@ -1,0 +1,562 @@
+// api.cu -- the C ABI of include/mf.h: operator setup, apply (with the z-slab
+// halo exchange over NCCL), diagonal, eigenvalue estimate, Chebyshev and the
+// preconditioned CG host loop (§8(a) a8-a10, §8(b)).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mf;
+
+struct mf_op {
+  Geo g;
+  Tables t;
+  int rank = 0, world = 1, device = 0;
+  cudaStream_t stream = 0;
+  int64_t n_local = 0, first_global = 0, n_global = 0, n_owned = 0, plane = 0;
+  int variant = kVariantAuto;
+  int64_t launches = 0;
+  double *metric = nullptr;  // [ncomp][cells][q] for MF_GEOM_SINE
+  // solver scratch (lazily allocated, n_local each)
+  double *diag = nullptr, *dinv = nullptr;
+  double *r = nullptr, *p = nullptr, *v = nullptr, *z = nullptr, *cd = nullptr, *cax = nullptr;
+  double *partials = nullptr, *dev_scal = nullptr, *host_scal = nullptr;
+  double *h_src = nullptr, *h_dst = nullptr;  // device buffers for mf_apply_host
+  double *recv_lo = nullptr, *recv_hi = nullptr;
+  ncclComm_t comm = nullptr;
+  // live kernel timing (mf_set_kernel_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // pairs (start, stop)
+  size_t ev_used = 0;
+};
+
+static thread_local std::string g_err;
+
+static mf_status fail(mf_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(call)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(e_ == cudaErrorMemoryAllocation ? MF_ERR_OUT_OF_MEMORY : MF_ERR_CUDA,      \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+#define NCCL_TRY(call)                                                                                   \
+  do {                                                                                                   \
+    ncclResult_t r_ = (call);                                                                            \
+    if (r_ != ncclSuccess) return fail(MF_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define STATUS_TRY(call)          \
+  do {                            \
+    mf_status s_ = (call);        \
+    if (s_ != MF_OK) return s_;   \
+  } while (0)
+
+extern "C" const char *mf_last_error(void) { return g_err.c_str(); }
+
+extern "C" mf_status mf_nccl_unique_id(uint8_t *out128) {
+  if (!out128) return fail(MF_ERR_ARGUMENT, "null output");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "NCCL unique id is 128 bytes");
+  std::memcpy(out128, &id, 128);
+  return MF_OK;
+}
+
+static int ncomp(int dim) { return dim == 3 ? 6 : 3; }
+static int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+static int64_t ncells_local(const Geo &g) { return g.nc[0] * g.nc[1] * (g.dim == 3 ? g.nc[2] : 1); }
+
+extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff, const mf_dist *dist,
+                               mf_op **out) {
+  if (!mesh || !coeff || !out) return fail(MF_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (mesh->dim != 2 && mesh->dim != 3) return fail(MF_ERR_ARGUMENT, "dim must be 2 or 3");
+  if (degree < 1 || degree > 8) return fail(MF_ERR_ARGUMENT, "degree must be in 1..8");
+  for (int e = 0; e < mesh->dim; ++e) {
+    if (mesh->n_cells[e] < 1) return fail(MF_ERR_ARGUMENT, "n_cells must be >= 1");
+    if (!(mesh->lower[e] < mesh->upper[e])) return fail(MF_ERR_ARGUMENT, "lower must be < upper");
+  }
+  if (mesh->geometry != MF_GEOM_CARTESIAN && mesh->geometry != MF_GEOM_SINE)
+    return fail(MF_ERR_ARGUMENT, "unknown geometry");
+  if (coeff->kind != MF_COEFF_CONSTANT && coeff->kind != MF_COEFF_VARIABLE)
+    return fail(MF_ERR_ARGUMENT, "unknown coefficient kind");
+  if (coeff->kind == MF_COEFF_CONSTANT && !(coeff->value > 0.0))
+    return fail(MF_ERR_ARGUMENT, "constant coefficient must be > 0");
+  int rank = 0, world = 1, device = -1;
+  if (dist) {
+    rank = dist->rank;
+    world = dist->world_size;
+    device = dist->device;
+    if (world < 1 || rank < 0 || rank >= world) return fail(MF_ERR_ARGUMENT, "bad rank/world_size");
+    if (world > 1 && (!dist->nccl_unique_id || mesh->dim != 3))
+      return fail(MF_ERR_ARGUMENT, "world_size > 1 needs dim 3 and an NCCL unique id");
+    if (world > 1 && mesh->n_cells[2] < world) return fail(MF_ERR_ARGUMENT, "fewer z cell layers than ranks");
+  }
+  if (device >= 0) CUDA_TRY(cudaSetDevice(device));
+  else CUDA_TRY(cudaGetDevice(&device));
+
+  mf_op *op = new mf_op();
+  op->rank = rank;
+  op->world = world;
+  op->device = device;
+  Geo &g = op->g;
+  std::memset(&g, 0, sizeof(Geo));
+  g.dim = mesh->dim;
+  g.k = degree;
+  for (int e = 0; e < 3; ++e) {
+    g.nc[e] = e < g.dim ? mesh->n_cells[e] : 1;
+    g.lo[e] = e < g.dim ? mesh->lower[e] : 0.0;
+    g.hi[e] = e < g.dim ? mesh->upper[e] : 1.0;
+    g.h[e] = (g.hi[e] - g.lo[e]) / (double)g.nc[e];
+  }
+  g.ncz_global = g.nc[2];
+  // z-slab of whole cell layers: rank r gets [r nz / P, (r+1) nz / P)
+  const int64_t cz0 = g.dim == 3 ? (int64_t)rank * g.nc[2] / world : 0;
+  const int64_t cz1 = g.dim == 3 ? (int64_t)(rank + 1) * g.nc[2] / world : 1;
+  g.cz0 = cz0;
+  if (g.dim == 3) g.nc[2] = cz1 - cz0;
+  for (int e = 0; e < 3; ++e) g.N[e] = e < g.dim ? (int64_t)degree * g.nc[e] + 1 : 1;
+  g.eps = mesh->deform_eps;
+  g.geom = mesh->geometry;
+  g.coeff_kind = coeff->kind;
+  g.coeff = coeff->value;
+  g.dirichlet = mesh->dirichlet_faces & ((1u << (2 * g.dim)) - 1u);
+  if (world > 1) {
+    if (rank > 0) g.dirichlet &= ~16u;
+    if (rank < world - 1) g.dirichlet &= ~32u;
+    g.skip_top_identity = rank < world - 1;
+  }
+  const double vol = g.h[0] * g.h[1] * (g.dim == 3 ? g.h[2] : 1.0);
+  for (int e = 0; e < g.dim; ++e) g.fcart[e] = coeff->value * vol / (g.h[e] * g.h[e]);
+  build_tables(degree, &op->t);
+
+  op->plane = g.N[0] * g.N[1];
+  op->n_local = g.N[0] * g.N[1] * g.N[2];
+  op->first_global = g.dim == 3 ? (int64_t)degree * cz0 * op->plane : 0;
+  op->n_global = g.dim == 3 ? op->plane * ((int64_t)degree * g.ncz_global + 1) : op->n_local;
+  op->n_owned = (world > 1 && rank < world - 1) ? op->n_local - op->plane : op->n_local;
+
+  auto cleanup = [&](mf_status s) {
+    mf_destroy(op);
+    return s;
+  };
+  if (cudaMallocHost(&op->host_scal, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->dev_scal, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->partials, 3 * kDotBlocks * sizeof(double)) != cudaSuccess)
+    return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "scalar buffers"));
+
+  if (g.geom == MF_GEOM_SINE) {
+    const int64_t nm = (int64_t)ncomp(g.dim) * ncells_local(g) * ipow(degree + 1, g.dim);
+    if (cudaMalloc(&op->metric, nm * sizeof(double)) != cudaSuccess)
+      return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "metric"));
+    int *bad = nullptr;
+    if (cudaMalloc(&bad, sizeof(int)) != cudaSuccess) return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "flag"));
+    cudaMemset(bad, 0, sizeof(int));
+    cudaError_t e = launch_metric(g, op->t, op->metric, bad, 0, &op->launches);
+    int hbad = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(bad);
+    if (e != cudaSuccess) return cleanup(fail(MF_ERR_CUDA, std::string("metric: ") + cudaGetErrorString(e)));
+    if (hbad) return cleanup(fail(MF_ERR_SINGULAR, "det J <= 0 at a quadrature point"));
+  }
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, dist->nccl_unique_id, 128);
+    ncclResult_t nr = ncclCommInitRank(&op->comm, world, id, rank);
+    if (nr != ncclSuccess) {
+      op->comm = nullptr;
+      return cleanup(fail(MF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr)));
+    }
+    if (cudaMalloc(&op->recv_lo, op->plane * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&op->recv_hi, op->plane * sizeof(double)) != cudaSuccess)
+      return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "halo buffers"));
+  }
+  *out = op;
+  return MF_OK;
+}
+
+extern "C" void mf_destroy(mf_op *op) {
+  if (!op) return;
+  cudaFree(op->metric);
+  for (double *b : {op->diag, op->dinv, op->r, op->p, op->v, op->z, op->cd, op->cax, op->partials, op->dev_scal,
+                    op->h_src, op->h_dst, op->recv_lo, op->recv_hi})
+    cudaFree(b);
+  if (op->host_scal) cudaFreeHost(op->host_scal);
+  for (cudaEvent_t e : op->ev) cudaEventDestroy(e);
+  if (op->comm) ncclCommDestroy(op->comm);
+  delete op;
+}
+
+extern "C" mf_status mf_sizes(const mf_op *op, int64_t *n_local, int64_t *first_global, int64_t *n_global,
+                              int64_t *n_owned) {
+  if (!op) return fail(MF_ERR_ARGUMENT, "null op");
+  if (n_local) *n_local = op->n_local;
+  if (first_global) *first_global = op->first_global;
+  if (n_global) *n_global = op->n_global;
+  if (n_owned) *n_owned = op->n_owned;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_set_stream(mf_op *op, void *s) {
+  if (!op) return fail(MF_ERR_ARGUMENT, "null op");
+  op->stream = (cudaStream_t)s;
+  return MF_OK;
+}
+
+static int chosen_variant(const mf_op *op) {
+  if (op->variant != kVariantAuto) return op->variant;
+  return cart_tile_supported(op->g) ? kVariantCartTile : kVariantGeneral;
+}
+
+extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
+  if (!op) return fail(MF_ERR_ARGUMENT, "null op");
+  if (variant == kVariantCartTile && !cart_tile_supported(op->g))
+    return fail(MF_ERR_ARGUMENT, "tile kernel needs dim 3, Cartesian geometry, constant coefficient");
+  if (variant < 0 || variant > kVariantCartTile) return fail(MF_ERR_ARGUMENT, "unknown variant");
+  op->variant = variant;
+  return MF_OK;
+}
+
+// symmetric exchange of the partial sums on shared z-planes (§8(e)):
+// send my partial of each shared plane, receive the neighbour's, add.
+static mf_status halo_exchange(mf_op *op, double *dst) {
+  if (op->world == 1) return MF_OK;
+  const int64_t np = op->plane;
+  double *lo = dst, *hi = dst + op->n_local - np;
+  const bool has_lo = op->rank > 0, has_hi = op->rank < op->world - 1;
+  NCCL_TRY(ncclGroupStart());
+  if (has_hi) {
+    NCCL_TRY(ncclSend(hi, np, ncclDouble, op->rank + 1, op->comm, op->stream));
+    NCCL_TRY(ncclRecv(op->recv_hi, np, ncclDouble, op->rank + 1, op->comm, op->stream));
+  }
+  if (has_lo) {
+    NCCL_TRY(ncclSend(lo, np, ncclDouble, op->rank - 1, op->comm, op->stream));
+    NCCL_TRY(ncclRecv(op->recv_lo, np, ncclDouble, op->rank - 1, op->comm, op->stream));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  if (has_hi) CUDA_TRY(launch_plane_add(hi, op->recv_hi, np, op->stream, &op->launches));
+  if (has_lo) CUDA_TRY(launch_plane_add(lo, op->recv_lo, np, op->stream, &op->launches));
+  return MF_OK;
+}
+
+static mf_status timing_mark(mf_op *op) {
+  if (!op->timing) return MF_OK;
+  if (op->ev_used == op->ev.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    op->ev.push_back(e);
+  }
+  CUDA_TRY(cudaEventRecord(op->ev[op->ev_used++], op->stream));
+  return MF_OK;
+}
+
+static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
+  const int var = chosen_variant(op);
+  if (var == kVariantCartTile) {
+    STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_apply_cart_tile(op->g, op->t, src, dst, op->stream, &op->launches));
+    STATUS_TRY(timing_mark(op));
+  } else {
+    CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
+    STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches));
+    STATUS_TRY(timing_mark(op));
+  }
+  return halo_exchange(op, dst);
+}
+
+extern "C" mf_status mf_set_kernel_timing(mf_op *op, int32_t enable) {
+  if (!op) return fail(MF_ERR_ARGUMENT, "null op");
+  op->timing = enable != 0;
+  op->ev_used = 0;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_kernel_timing(mf_op *op, double *ms_total, int64_t *count) {
+  if (!op || !ms_total || !count) return fail(MF_ERR_ARGUMENT, "null argument");
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < op->ev_used; i += 2) {
+    CUDA_TRY(cudaEventSynchronize(op->ev[i + 1]));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, op->ev[i], op->ev[i + 1]));
+    total += ms;
+  }
+  *ms_total = total;
+  *count = (int64_t)(op->ev_used / 2);
+  return MF_OK;
+}
+
+extern "C" mf_status mf_apply(mf_op *op, const double *src, int64_t n_src, double *dst, int64_t n_dst) {
+  if (!op || !src || !dst) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n_src != op->n_local || n_dst != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  if (src == dst) return fail(MF_ERR_ARGUMENT, "src and dst must be distinct");
+  return apply_impl(op, src, dst);
+}
+
+extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_src, double *dst_host,
+                                   int64_t n_dst) {
+  if (!op || !src_host || !dst_host) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n_src != op->n_local || n_dst != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  const size_t bytes = op->n_local * sizeof(double);
+  if (!op->h_src) {
+    CUDA_TRY(cudaMalloc(&op->h_src, bytes));
+    CUDA_TRY(cudaMalloc(&op->h_dst, bytes));
+  }
+  CUDA_TRY(cudaMemcpyAsync(op->h_src, src_host, bytes, cudaMemcpyHostToDevice, op->stream));
+  STATUS_TRY(apply_impl(op, op->h_src, op->h_dst));
+  CUDA_TRY(cudaMemcpyAsync(dst_host, op->h_dst, bytes, cudaMemcpyDeviceToHost, op->stream));
+  CUDA_TRY(cudaStreamSynchronize(op->stream));
+  return MF_OK;
+}
+
+static mf_status diagonal_impl(mf_op *op, double *diag) {
+  CUDA_TRY(launch_zero(diag, op->n_local, op->stream, &op->launches));
+  CUDA_TRY(launch_diagonal(op->g, op->t, diag, op->metric, op->stream, &op->launches));
+  return halo_exchange(op, diag);
+}
+
+extern "C" mf_status mf_diagonal(mf_op *op, double *diag, int64_t n) {
+  if (!op || !diag) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  return diagonal_impl(op, diag);
+}
+
+static mf_status ensure_solver(mf_op *op) {
+  if (op->r) return MF_OK;
+  const size_t bytes = op->n_local * sizeof(double);
+  for (double **b : {&op->diag, &op->dinv, &op->r, &op->p, &op->v, &op->z, &op->cd, &op->cax})
+    CUDA_TRY(cudaMalloc(b, bytes));
+  STATUS_TRY(diagonal_impl(op, op->diag));
+  CUDA_TRY(launch_recip(op->diag, op->dinv, op->n_local, op->stream, &op->launches));
+  return MF_OK;
+}
+
+// nd dot products over the owned prefix, summed over ranks; result to host_scal[0..nd)
+static mf_status dots(mf_op *op, int nd, const double *const *a, const double *const *b) {
+  CUDA_TRY(launch_dots(nd, a, b, op->n_owned, op->partials, op->dev_scal, op->stream, &op->launches));
+  if (op->world > 1)
+    NCCL_TRY(ncclAllReduce(op->dev_scal, op->dev_scal, nd, ncclDouble, ncclSum, op->comm, op->stream));
+  CUDA_TRY(cudaMemcpyAsync(op->host_scal, op->dev_scal, nd * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+  CUDA_TRY(cudaStreamSynchronize(op->stream));
+  return MF_OK;
+}
+
+// largest eigenvalue of the symmetric tridiagonal (d, e) by Sturm-sequence bisection
+static double tridiag_max_eig(const std::vector<double> &d, const std::vector<double> &e) {
+  const int m = (int)d.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < m; ++i) {
+    double r = (i > 0 ? std::fabs(e[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(e[i]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+  }
+  auto count_below = [&](double x) {
+    int c = 0;
+    double q = 1.0;
+    for (int i = 0; i < m; ++i) {
+      q = d[i] - x - (i > 0 ? e[i - 1] * e[i - 1] / q : 0.0);
+      if (q == 0.0) q = -1e-300;
+      if (q < 0.0) ++c;
+    }
+    return c;
+  };
+  for (int it = 0; it < 200 && hi - lo > 1e-16 * std::max(std::fabs(hi), std::fabs(lo)); ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (count_below(mid) >= m) hi = mid;
+    else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// O10 / S:639-647, with the reading of DESIGN.md R8
+static mf_status lambda_impl(mf_op *op, int steps, double *lam) {
+  STATUS_TRY(ensure_solver(op));
+  const int64_t n = op->n_local;
+  cudaStream_t s = op->stream;
+  double *r = op->r, *z = op->z, *p = op->p, *v = op->v;
+  CUDA_TRY(launch_splitmix(r, n, op->first_global, 0, s, &op->launches));
+  CUDA_TRY(launch_set_constrained(op->g, r, 0.0, s, &op->launches));
+  CUDA_TRY(launch_mul(op->dinv, r, z, n, s, &op->launches));
+  CUDA_TRY(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  {
+    const double *a[1] = {r}, *b[1] = {z};
+    STATUS_TRY(dots(op, 1, a, b));
+  }
+  double rz = op->host_scal[0];
+  const double rz0 = rz;
+  std::vector<double> al, be;
+  for (int j = 0; j < steps; ++j) {
+    STATUS_TRY(apply_impl(op, p, v));
+    const double *a[1] = {p}, *b[1] = {v};
+    STATUS_TRY(dots(op, 1, a, b));
+    const double pv = op->host_scal[0];
+    if (!(pv > 0.0)) return fail(MF_ERR_BREAKDOWN, "p.Ap <= 0 in eigenvalue estimate");
+    const double alpha = rz / pv;
+    al.push_back(alpha);
+    CUDA_TRY(launch_axpby(-alpha, v, 1.0, r, n, s, &op->launches));
+    CUDA_TRY(launch_mul(op->dinv, r, z, n, s, &op->launches));
+    const double *a2[1] = {r}, *b2[1] = {z};
+    STATUS_TRY(dots(op, 1, a2, b2));
+    const double rzn = op->host_scal[0];
+    if (rzn <= 1e-28 * rz0) break;
+    const double beta = rzn / rz;
+    be.push_back(beta);
+    CUDA_TRY(launch_axpby(1.0, z, beta, p, n, s, &op->launches));
+    rz = rzn;
+  }
+  const int m = (int)al.size();
+  std::vector<double> d(m), e(m > 0 ? m - 1 : 0);
+  for (int j = 0; j < m; ++j) {
+    d[j] = 1.0 / al[j] + (j > 0 ? be[j - 1] / al[j - 1] : 0.0);
+    if (j + 1 < m) e[j] = std::sqrt(be[j]) / al[j];
+  }
+  *lam = m > 0 ? tridiag_max_eig(d, e) : 0.0;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_estimate_lambda_max(mf_op *op, int32_t steps, double *lambda_out) {
+  if (!op || !lambda_out || steps < 1) return fail(MF_ERR_ARGUMENT, "bad argument");
+  return lambda_impl(op, steps, lambda_out);
+}
+
+// O11 / S:648-656: z = Chebyshev(degree) for D^{-1}A on [lam/range, lam] from 0
+static mf_status cheb_impl(mf_op *op, const double *r, double *x, double lam, int degree, double range) {
+  STATUS_TRY(ensure_solver(op));
+  const int64_t n = op->n_local;
+  const double a = lam / range, b = lam;
+  const double theta = 0.5 * (a + b), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  CUDA_TRY(launch_cheb_init(r, op->dinv, 1.0 / theta, x, op->cd, n, op->stream, &op->launches));
+  for (int j = 1; j < degree; ++j) {
+    const double rho_n = 1.0 / (2.0 * sigma - rho);
+    STATUS_TRY(apply_impl(op, x, op->cax));
+    CUDA_TRY(launch_cheb_step(r, op->cax, op->dinv, rho_n * rho, 2.0 * rho_n / delta, x, op->cd, n, op->stream,
+                              &op->launches));
+    rho = rho_n;
+  }
+  return MF_OK;
+}
+
+extern "C" mf_status mf_chebyshev(mf_op *op, const double *r, double *z, int64_t n, double lambda, int32_t degree,
+                                  double smoothing_range) {
+  if (!op || !r || !z) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  if (degree < 1 || !(lambda > 0.0) || !(smoothing_range > 1.0)) return fail(MF_ERR_ARGUMENT, "bad parameters");
+  return cheb_impl(op, r, z, lambda, degree, smoothing_range);
+}
+
+// O9 / S:500-508: PCG from x0 = 0 with P = Chebyshev(cheb_degree) (or Jacobi if 0)
+extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t n, const mf_cg_params *prm,
+                                 mf_cg_result *res, double *history, int32_t history_cap) {
+  if (!op || !b || !x || !prm || !res) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  if (!(prm->rel_tol > 0.0) || prm->max_iter < 1) return fail(MF_ERR_ARGUMENT, "bad CG parameters");
+  STATUS_TRY(ensure_solver(op));
+  cudaStream_t s = op->stream;
+  double *r = op->r, *p = op->p, *v = op->v, *z = op->z;
+  res->iterations = 0;
+  res->final_rel_residual = 0.0;
+  res->lambda_max = 0.0;
+  double lam = 0.0;
+  if (prm->cheb_degree > 0) {
+    STATUS_TRY(lambda_impl(op, prm->eig_cg_steps, &lam));
+    lam *= prm->cheb_safety;
+    res->lambda_max = lam;
+  }
+  auto precond = [&](const double *rr, double *zz) -> mf_status {
+    if (prm->cheb_degree > 0) return cheb_impl(op, rr, zz, lam, prm->cheb_degree, prm->cheb_range);
+    CUDA_TRY(launch_mul(op->dinv, rr, zz, n, s, &op->launches));
+    return MF_OK;
+  };
+  CUDA_TRY(launch_zero(x, n, s, &op->launches));
+  CUDA_TRY(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  {
+    const double *a[1] = {b}, *bb[1] = {b};
+    STATUS_TRY(dots(op, 1, a, bb));
+  }
+  const double normb = std::sqrt(op->host_scal[0]);
+  if (normb == 0.0) return MF_OK;
+  STATUS_TRY(precond(r, z));
+  CUDA_TRY(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  {
+    const double *a[1] = {r}, *bb[1] = {z};
+    STATUS_TRY(dots(op, 1, a, bb));
+  }
+  double rz = op->host_scal[0];
+  int it = 0;
+  while (true) {
+    STATUS_TRY(apply_impl(op, p, v));
+    ++it;
+    {
+      const double *a[1] = {p}, *bb[1] = {v};
+      STATUS_TRY(dots(op, 1, a, bb));
+    }
+    const double pv = op->host_scal[0];
+    if (!(pv > 0.0)) {
+      res->iterations = it;
+      return fail(MF_ERR_BREAKDOWN, "p.Ap <= 0");
+    }
+    op->host_scal[4] = rz / pv;
+    CUDA_TRY(cudaMemcpyAsync(op->dev_scal + 4, op->host_scal + 4, sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(launch_cg_update_xr(op->dev_scal + 4, x, r, p, v, n, s, &op->launches));
+    {
+      const double *a[1] = {r}, *bb[1] = {r};
+      STATUS_TRY(dots(op, 1, a, bb));
+    }
+    const double resn = std::sqrt(op->host_scal[0]);
+    if (history && it <= history_cap) history[it - 1] = resn;
+    res->iterations = it;
+    res->final_rel_residual = resn / normb;
+    if (resn <= prm->rel_tol * normb) return MF_OK;
+    if (it >= prm->max_iter) return fail(MF_ERR_MAX_ITERATIONS, "CG did not converge");
+    STATUS_TRY(precond(r, z));
+    {
+      const double *a[1] = {r}, *bb[1] = {z};
+      STATUS_TRY(dots(op, 1, a, bb));
+    }
+    const double rzn = op->host_scal[0];
+    if (!(rzn > 0.0)) return fail(MF_ERR_BREAKDOWN, "r.z <= 0");
+    op->host_scal[5] = rzn / rz;
+    CUDA_TRY(cudaMemcpyAsync(op->dev_scal + 5, op->host_scal + 5, sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(launch_cg_update_p(op->dev_scal + 5, z, p, n, s, &op->launches));
+    rz = rzn;
+  }
+}
+
+extern "C" mf_status mf_get_info(const mf_op *op, mf_info *info) {
+  if (!op || !info) return fail(MF_ERR_ARGUMENT, "null argument");
+  const Geo &g = op->g;
+  info->dim = g.dim;
+  info->degree = g.k;
+  info->geometry = g.geom;
+  info->coeff_kind = g.coeff_kind;
+  info->apply_variant = chosen_variant(op);
+  info->n_cells_local = ncells_local(g);
+  info->kernel_launches = op->launches;
+  const int64_t nq = ipow(g.k + 1, g.dim);
+  info->bytes_algorithmic =
+      16 * op->n_local + (g.geom == MF_GEOM_SINE ? 8 * (int64_t)ncomp(g.dim) * ncells_local(g) * nq : 0);
+  // 12-sweep (3D) / 8-sweep (2D) collocation kernel: 2 * (2 dim sweeps) * N^{dim+1} FMA + q-point op
+  const double N = g.k + 1;
+  const double sweeps = 4.0 * g.dim;
+  const double qop = g.geom == MF_GEOM_SINE ? 2.0 * g.dim * g.dim : 2.0 * g.dim;
+  info->flops_algorithmic =
+      (double)ncells_local(g) * (2.0 * sweeps * std::pow(N, g.dim + 1) + qop * std::pow(N, g.dim));
+  return MF_OK;
+}

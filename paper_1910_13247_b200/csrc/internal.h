@@ -1,0 +1,95 @@
+// internal.h -- shared declarations of libmf_b200 (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <string>
+
+#include "../../include/mf.h"
+
+namespace mf {
+
+constexpr int kMaxN = 9;  // k <= 8
+
+// 1D tables on [0,1] for degree k (n = k+1 nodes = Gauss points), passed to
+// kernels BY VALUE so they live in the constant bank (DFMA c[0x0][...] operands).
+//   S[q][i]   = l_i(xi_q)         GLL Lagrange basis at Gauss point q
+//   D[q][i]   = l_i'(xi_q)        its derivative (metric / diagonal kernels)
+//   Co[q][p]  = lG_p'(xi_q)       collocation derivative on the Gauss points
+//   w[q]      Gauss weights
+struct Tables {
+  double S[kMaxN][kMaxN];
+  double D[kMaxN][kMaxN];
+  double Co[kMaxN][kMaxN];
+  double w[kMaxN];
+  double gll[kMaxN];
+  double xi[kMaxN];
+};
+
+// Host-side construction (tables.cpp): an implementation of the 1D rules
+// written independently of oracle/ (long double Newton iterations).
+void build_tables(int k, Tables *t);
+
+// Geometry / coefficient description shared by the kernels.
+struct Geo {
+  int dim, k;
+  int64_t nc[3];        // local cells per direction (z local for slabs)
+  int64_t N[3];         // local nodes per direction
+  int64_t cz0;          // global z offset of the local slab (in cells)
+  int64_t ncz_global;
+  double lo[3], hi[3], h[3];
+  double eps;
+  int geom;             // MF_GEOM_*
+  int coeff_kind;       // MF_COEFF_*
+  double coeff;         // constant value
+  uint32_t dirichlet;   // face bits, with z faces masked for inner slab boundaries
+  int skip_top_identity;  // lower rank of a shared top plane: upper rank writes the identity rows there
+  double fcart[3];      // c * prod(h) / h_e^2 (Cartesian, constant coefficient)
+};
+
+enum Variant {
+  kVariantAuto = 0,
+  kVariantGeneral = 1,  // 12-sweep collocation kernel, any dim/k/geometry
+  kVariantCartTile = 2, // Cartesian constant-coefficient 3D tile kernel
+};
+
+// Kernel launchers (return cudaError_t of the launch).
+cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
+                                 const double *metric, cudaStream_t s, int64_t *launches);
+cudaError_t launch_apply_cart_tile(const Geo &g, const Tables &t, const double *src, double *dst,
+                                   cudaStream_t s, int64_t *launches);
+bool cart_tile_supported(const Geo &g);
+cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
+                          int64_t *launches);
+cudaError_t launch_diagonal(const Geo &g, const Tables &t, double *diag, const double *metric,
+                            cudaStream_t s, int64_t *launches);
+cudaError_t launch_zero(double *x, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_set_constrained(const Geo &g, double *x, double value, cudaStream_t s, int64_t *launches);
+
+// vector kernels (kernels_vec.cu)
+cudaError_t launch_splitmix(double *x, int64_t n, int64_t first_global, uint64_t seed, cudaStream_t s,
+                            int64_t *launches);
+// partial dot products into `partials` (fixed block count), then a second pass into out[j]
+cudaError_t launch_dots(int ndots, const double *const *a, const double *const *b, int64_t n,
+                        double *partials, double *out, cudaStream_t s, int64_t *launches);
+// y = a*x + b*y   (and variants used by CG / Chebyshev)
+cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n, cudaStream_t s,
+                         int64_t *launches);
+// CG update with device scalars: alpha = num/den -> x += alpha p, r -= alpha v
+cudaError_t launch_cg_update_xr(const double *scal, double *x, double *r, const double *p, const double *v,
+                                int64_t n, cudaStream_t s, int64_t *launches);
+// p = z + beta p, beta = scal
+cudaError_t launch_cg_update_p(const double *beta, const double *z, double *p, int64_t n, cudaStream_t s,
+                               int64_t *launches);
+// Chebyshev: first step x = dinv*r*c0 (d = x), later d = c1*d + c2*dinv*(r - Ax); x += d
+cudaError_t launch_cheb_init(const double *r, const double *dinv, double c0, double *x, double *d, int64_t n,
+                             cudaStream_t s, int64_t *launches);
+cudaError_t launch_cheb_step(const double *r, const double *ax, const double *dinv, double c1, double c2,
+                             double *x, double *d, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_mul(const double *a, const double *b, double *out, int64_t n, cudaStream_t s,
+                       int64_t *launches);
+cudaError_t launch_recip(const double *x, double *y, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_plane_add(double *dst, const double *recv, int64_t n, cudaStream_t s, int64_t *launches);
+
+constexpr int kDotBlocks = 592;  // 4 x 148 SMs
+
+}  // namespace mf

@@ -1,0 +1,597 @@
+// kernels_general.cu -- the general matrix-free cell kernel (any dim in {2,3},
+// degree k in 1..8, Cartesian or curved geometry, constant or variable
+// coefficient), the metric precompute and the operator diagonal.
+//
+// Method (§3.6):
+//   a3 gather the (k+1)^d cell values (Dirichlet DoFs read as 0),
+//   a4 sum factorisation to the Gauss points: Q = (S (x) S (x) S) u, then the
+//      reference gradient g_e = Co along e applied to Q (collocation derivative),
+//   a5 quadrature-point operation t = G_q g  (G_q = c w |det J| J^{-1} J^{-T};
+//      for affine boxes t_e = c w_q prod(h)/h_e^2 g_e),
+//   a6 transposed sweeps R = sum_e Co^T_e t_e, v = (S^T (x) S^T (x) S^T) R,
+//   a7 scatter-add (FP64 atomics into a zeroed dst) and the Dirichlet identity
+//      dst_g = src_g, written once per constrained DoF by its owner cell.
+// One thread block handles a batch of `cpb` consecutive cells (the
+// GPU analogue of the SIMD cell batch); each thread owns one pencil of n values
+// per sweep (thread-per-pencil, not the thread-per-DoF of P:960-961, whose
+// n^4 shared-memory reads per sweep the pencil form avoids).  The 1D tables are
+// a __grid_constant__ kernel parameter, so every matrix entry is a constant-bank
+// operand of the DFMA.
+#include <cstdio>
+
+#include "internal.h"
+
+namespace mf {
+
+template <int DIM, int N>
+struct Shape {
+  static constexpr int NP = DIM == 3 ? N * N : N;  // pencils per direction
+  static constexpr int NV = NP * N;                // values per cell
+};
+
+// offset of entry i of pencil p along direction dir inside an N^DIM cell tensor (x fastest)
+template <int DIM, int N>
+__device__ __forceinline__ int pen_off(int dir, int p, int i) {
+  if (DIM == 2) return dir == 0 ? p * N + i : i * N + p;
+  if (dir == 0) return p * N + i;                          // p = z*N + y
+  if (dir == 1) return (p / N) * N * N + i * N + (p % N);  // p = z*N + x
+  return i * N * N + p;                                    // p = y*N + x
+}
+
+// out[i] = sum_j M[i][j] in[j]   (TR: sum_j M[j][i] in[j])
+template <int N, bool TR>
+__device__ __forceinline__ void mat1d(const double (&M)[kMaxN][kMaxN], const double *in, double *out) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(TR ? M[j][i] : M[i][j], in[j], s);
+    out[i] = s;
+  }
+}
+
+template <int DIM, int N, bool TR>
+__device__ __forceinline__ void sweep_inplace(const double (&M)[kMaxN][kMaxN], double *U, int dir, int p) {
+  double a[N], b[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = U[pen_off<DIM, N>(dir, p, i)];
+  mat1d<N, TR>(M, a, b);
+#pragma unroll
+  for (int i = 0; i < N; ++i) U[pen_off<DIM, N>(dir, p, i)] = b[i];
+}
+
+struct CellIdx {
+  int64_t c[3];
+};
+
+__device__ __forceinline__ CellIdx cell_coords(const Geo &g, int64_t cell) {
+  CellIdx ci;
+  ci.c[0] = cell % g.nc[0];
+  int64_t r = cell / g.nc[0];
+  ci.c[1] = r % g.nc[1];
+  ci.c[2] = r / g.nc[1];
+  return ci;
+}
+
+// local node (l) of cell (c) -> global node coords and local DoF index; constrained flag
+template <int DIM, int N>
+__device__ __forceinline__ int64_t node_index(const Geo &g, const CellIdx &ci, int i, int64_t m[3]) {
+  const int K = N - 1;
+  int l0 = i % N, l1 = DIM >= 2 ? (i / N) % N : 0, l2 = DIM == 3 ? i / (N * N) : 0;
+  m[0] = K * ci.c[0] + l0;
+  m[1] = K * ci.c[1] + l1;
+  m[2] = DIM == 3 ? K * ci.c[2] + l2 : 0;
+  return (m[2] * g.N[1] + m[1]) * g.N[0] + m[0];
+}
+
+__device__ __forceinline__ bool is_constrained(const Geo &g, const int64_t m[3]) {
+  const uint32_t d = g.dirichlet;
+  return ((d & 1u) && m[0] == 0) || ((d & 2u) && m[0] == g.N[0] - 1) || ((d & 4u) && m[1] == 0) ||
+         ((d & 8u) && m[1] == g.N[1] - 1) || ((d & 16u) && m[2] == 0) || ((d & 32u) && m[2] == g.N[2] - 1);
+}
+
+// The cell that writes the identity row of a constrained node: local index
+// >= 1 in every direction unless the node is on the low end of the brick.
+template <int DIM, int N>
+__device__ __forceinline__ bool owner_of(const Geo &g, const CellIdx &ci, int i, const int64_t m[3]) {
+  int l0 = i % N, l1 = (i / N) % N, l2 = DIM == 3 ? i / (N * N) : 1;
+  bool own = (l0 >= 1 || ci.c[0] == 0) && (l1 >= 1 || ci.c[1] == 0) && (DIM == 2 || l2 >= 1 || ci.c[2] == 0);
+  if (g.skip_top_identity && DIM == 3 && m[2] == g.N[2] - 1) own = false;
+  return own;
+}
+
+__device__ __forceinline__ double coeff_var(const double x[3], int dim) {
+  double r2 = 0.0;
+  for (int d = 0; d < dim; ++d) r2 += x[d] * x[d];
+  return 1.0 / (0.05 + 2.0 * r2);  // R5
+}
+
+// ---------------------------------------------------------------------------
+// GEOM: 0 = affine box, constant coefficient; 1 = affine box, variable
+// coefficient evaluated at x_q on the fly; 2 = stored metric G (curved).
+template <int DIM, int K, int GEOM>
+__global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ Tables t,
+                                                       const __grid_constant__ Geo g,
+                                                       const double *__restrict__ src, double *__restrict__ dst,
+                                                       const double *__restrict__ metric, int cpb) {
+  constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
+  constexpr int CS = (DIM + 1) * NV;  // doubles of shared memory per cell
+  extern __shared__ double sm[];
+  const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
+  const int64_t cell0 = (int64_t)blockIdx.x * cpb;
+
+  // a3: gather
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int cl = idx / NV, i = idx - cl * NV;
+    const int64_t cell = cell0 + cl;
+    double v = 0.0;
+    if (cell < ncells) {
+      CellIdx ci = cell_coords(g, cell);
+      int64_t m[3];
+      int64_t gi = node_index<DIM, N>(g, ci, i, m);
+      if (!is_constrained(g, m)) v = __ldg(src + gi);
+    }
+    sm[cl * CS + i] = v;
+  }
+  __syncthreads();
+
+  const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
+  const bool active = cl < cpb;
+  double *U = sm + cl * CS;
+
+  // a4: values at Gauss points, one direction at a time
+#pragma unroll
+  for (int e = 0; e < DIM; ++e) {
+    if (active) sweep_inplace<DIM, N, false>(t.S, U, e, p);
+    __syncthreads();
+  }
+  // reference gradient by collocation derivative along each direction
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) {
+      double a[N], b[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) a[i] = U[pen_off<DIM, N>(e, p, i)];
+      mat1d<N, false>(t.Co, a, b);
+      double *G = U + (e + 1) * NV;
+#pragma unroll
+      for (int i = 0; i < N; ++i) G[pen_off<DIM, N>(e, p, i)] = b[i];
+    }
+  }
+  __syncthreads();
+
+  // a5: quadrature-point operation
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int c2 = idx / NV, q = idx - c2 * NV;
+    const int64_t cell = cell0 + c2;
+    double *Uc = sm + c2 * CS;
+    const int q0 = q % N, q1 = (q / N) % N, q2 = DIM == 3 ? q / (N * N) : 0;
+    double gr[3], tt[3];
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) gr[e] = Uc[(e + 1) * NV + q];
+    if (GEOM == 2) {
+      if (cell < ncells) {
+        const int64_t stride = ncells * NV;
+        const double *Gm = metric + cell * NV + q;
+        if (DIM == 3) {
+          double G00 = __ldg(Gm), G01 = __ldg(Gm + stride), G02 = __ldg(Gm + 2 * stride),
+                 G11 = __ldg(Gm + 3 * stride), G12 = __ldg(Gm + 4 * stride), G22 = __ldg(Gm + 5 * stride);
+          tt[0] = G00 * gr[0] + G01 * gr[1] + G02 * gr[2];
+          tt[1] = G01 * gr[0] + G11 * gr[1] + G12 * gr[2];
+          tt[2] = G02 * gr[0] + G12 * gr[1] + G22 * gr[2];
+        } else {
+          double G00 = __ldg(Gm), G01 = __ldg(Gm + stride), G11 = __ldg(Gm + 2 * stride);
+          tt[0] = G00 * gr[0] + G01 * gr[1];
+          tt[1] = G01 * gr[0] + G11 * gr[1];
+        }
+      } else {
+        tt[0] = tt[1] = tt[2] = 0.0;
+      }
+    } else {
+      double W = t.w[q0] * t.w[q1] * (DIM == 3 ? t.w[q2] : 1.0);
+      if (GEOM == 1) {
+        CellIdx ci = cell_coords(g, cell < ncells ? cell : 0);
+        double x[3];
+        const int qq[3] = {q0, q1, q2};
+        for (int d = 0; d < DIM; ++d) {
+          double cg = (double)(d == 2 ? ci.c[2] + g.cz0 : ci.c[d]);
+          x[d] = g.lo[d] + g.h[d] * (cg + t.xi[qq[d]]);
+        }
+        double vol = g.h[0] * g.h[1] * (DIM == 3 ? g.h[2] : 1.0);
+        W *= coeff_var(x, DIM) * vol;
+#pragma unroll
+        for (int e = 0; e < DIM; ++e) tt[e] = W / (g.h[e] * g.h[e]) * gr[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < DIM; ++e) tt[e] = W * g.fcart[e] * gr[e];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) Uc[(e + 1) * NV + q] = tt[e];
+  }
+  __syncthreads();
+
+  // a6: transposed collocation derivative (in place, one array per direction)
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) sweep_inplace<DIM, N, true>(t.Co, U + (e + 1) * NV, e, p);
+  }
+  __syncthreads();
+  // sum the directions and apply S^T along x
+  if (active) {
+    double a[N], b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int o = pen_off<DIM, N>(0, p, i);
+      double s = U[NV + o];
+#pragma unroll
+      for (int e = 1; e < DIM; ++e) s += U[(e + 1) * NV + o];
+      a[i] = s;
+    }
+    mat1d<N, true>(t.S, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) U[pen_off<DIM, N>(0, p, i)] = b[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 1; e < DIM; ++e) {
+    if (active) sweep_inplace<DIM, N, true>(t.S, U, e, p);
+    __syncthreads();
+  }
+
+  // a7: scatter-add and identity rows
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int c2 = idx / NV, i = idx - c2 * NV;
+    const int64_t cell = cell0 + c2;
+    if (cell >= ncells) continue;
+    CellIdx ci = cell_coords(g, cell);
+    int64_t m[3];
+    int64_t gi = node_index<DIM, N>(g, ci, i, m);
+    if (is_constrained(g, m)) {
+      if (owner_of<DIM, N>(g, ci, i, m)) dst[gi] = __ldg(src + gi);
+    } else {
+      atomicAdd(dst + gi, sm[c2 * CS + i]);
+    }
+  }
+}
+
+template <int DIM, int K>
+static int cells_per_block() {
+  constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
+  int cpb = 256 / NP;
+  const int cs = (DIM + 1) * NV * 8;
+  while (cpb > 1 && cpb * cs > 48 * 1024) --cpb;
+  return cpb < 1 ? 1 : cpb;
+}
+
+template <int DIM, int K, int GEOM>
+static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double *src, double *dst,
+                                    const double *metric, cudaStream_t s) {
+  constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
+  const int cpb = cells_per_block<DIM, K>();
+  int threads = ((cpb * NP + 31) / 32) * 32;
+  const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
+  const int64_t blocks = (ncells + cpb - 1) / cpb;
+  const size_t smem = (size_t)cpb * (DIM + 1) * NV * sizeof(double);
+  if (blocks == 0) return cudaSuccess;
+  k_apply_general<DIM, K, GEOM><<<(unsigned)blocks, threads, smem, s>>>(t, g, src, dst, metric, cpb);
+  return cudaGetLastError();
+}
+
+template <int DIM, int GEOM>
+static cudaError_t dispatch_k(const Geo &g, const Tables &t, const double *src, double *dst,
+                              const double *metric, cudaStream_t s) {
+  switch (g.k) {
+    case 1: return launch_general_t<DIM, 1, GEOM>(g, t, src, dst, metric, s);
+    case 2: return launch_general_t<DIM, 2, GEOM>(g, t, src, dst, metric, s);
+    case 3: return launch_general_t<DIM, 3, GEOM>(g, t, src, dst, metric, s);
+    case 4: return launch_general_t<DIM, 4, GEOM>(g, t, src, dst, metric, s);
+    case 5: return launch_general_t<DIM, 5, GEOM>(g, t, src, dst, metric, s);
+    case 6: return launch_general_t<DIM, 6, GEOM>(g, t, src, dst, metric, s);
+    case 7: return launch_general_t<DIM, 7, GEOM>(g, t, src, dst, metric, s);
+    case 8: return launch_general_t<DIM, 8, GEOM>(g, t, src, dst, metric, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+static int geom_kind(const Geo &g) {
+  if (g.geom == MF_GEOM_SINE) return 2;
+  return g.coeff_kind == MF_COEFF_VARIABLE ? 1 : 0;
+}
+
+cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
+                                 const double *metric, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  const int gk = geom_kind(g);
+  if (g.dim == 2) {
+    if (gk == 0) return dispatch_k<2, 0>(g, t, src, dst, metric, s);
+    if (gk == 1) return dispatch_k<2, 1>(g, t, src, dst, metric, s);
+    return dispatch_k<2, 2>(g, t, src, dst, metric, s);
+  }
+  if (gk == 0) return dispatch_k<3, 0>(g, t, src, dst, metric, s);
+  if (gk == 1) return dispatch_k<3, 1>(g, t, src, dst, metric, s);
+  return dispatch_k<3, 2>(g, t, src, dst, metric, s);
+}
+
+// ---------------------------------------------------------------------------
+// Metric precompute (§8(a) a2): per cell and Gauss point, the isoparametric
+// Jacobian J = sum_j x_j (x) grad-hat psi_j(xi_q) from the support points
+// x_j = Phi(GLL node) (R4, H8), x_q = sum_j x_j psi_j(xi_q), and
+// G = c(x_q) w_q det J J^{-1} J^{-T}, stored SoA [comp][cell][q]
+// (3D comps: 00 01 02 11 12 22; 2D: 00 01 11).  det J <= 0 sets *bad.
+// One block per cell; thread = Gauss point.  Setup only (brute-force sums).
+template <int DIM, int K>
+__global__ void k_metric(const __grid_constant__ Tables t, const __grid_constant__ Geo g, double *metric,
+                         int *bad) {
+  constexpr int N = K + 1, NV = Shape<DIM, N>::NV;
+  __shared__ double X[NV][3];
+  const int64_t cell = blockIdx.x;
+  const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
+  CellIdx ci = cell_coords(g, cell);
+  for (int j = threadIdx.x; j < NV; j += blockDim.x) {
+    const int l[3] = {j % N, (j / N) % N, DIM == 3 ? j / (N * N) : 0};
+    double xb[3], s = 1.0;
+    for (int d = 0; d < DIM; ++d) {
+      double cg = (double)(d == 2 ? ci.c[2] + g.cz0 : ci.c[d]);
+      xb[d] = g.lo[d] + g.h[d] * (cg + t.gll[l[d]]);
+      s *= sin(M_PI * (xb[d] - g.lo[d]) / (g.hi[d] - g.lo[d]));
+    }
+    for (int d = 0; d < DIM; ++d)
+      X[j][d] = xb[d] + (g.geom == MF_GEOM_SINE ? g.eps * (g.hi[d] - g.lo[d]) * s : 0.0);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+    const int qd[3] = {q % N, (q / N) % N, DIM == 3 ? q / (N * N) : 0};
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, x[3] = {0, 0, 0};
+    for (int j = 0; j < NV; ++j) {
+      const int l[3] = {j % N, (j / N) % N, DIM == 3 ? j / (N * N) : 0};
+      double sv[3], dv[3];
+      for (int d = 0; d < DIM; ++d) {
+        sv[d] = t.S[qd[d]][l[d]];
+        dv[d] = t.D[qd[d]][l[d]];
+      }
+      double psi = sv[0] * sv[1] * (DIM == 3 ? sv[2] : 1.0);
+      double gr[3];
+      gr[0] = dv[0] * sv[1] * (DIM == 3 ? sv[2] : 1.0);
+      gr[1] = sv[0] * dv[1] * (DIM == 3 ? sv[2] : 1.0);
+      gr[2] = DIM == 3 ? sv[0] * sv[1] * dv[2] : 0.0;
+      for (int a = 0; a < DIM; ++a) {
+        x[a] += X[j][a] * psi;
+        for (int b = 0; b < DIM; ++b) J[a][b] += X[j][a] * gr[b];
+      }
+    }
+    double W = t.w[qd[0]] * t.w[qd[1]] * (DIM == 3 ? t.w[qd[2]] : 1.0);
+    double c = g.coeff_kind == MF_COEFF_VARIABLE ? coeff_var(x, DIM) : g.coeff;
+    const int64_t stride = ncells * NV;
+    double *out = metric + cell * NV + q;
+    if (DIM == 3) {
+      double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+             C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      double det = J[0][0] * C00 + J[0][1] * C01 + J[0][2] * C02;
+      if (!(det > 0.0)) atomicOr(bad, 1);
+      double Ji[3][3];  // inverse
+      Ji[0][0] = C00 / det;
+      Ji[1][0] = C01 / det;
+      Ji[2][0] = C02 / det;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+      const double f = c * W * det;
+      int o = 0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = a; b < 3; ++b) {
+          double s = 0.0;
+          for (int m = 0; m < 3; ++m) s += Ji[a][m] * Ji[b][m];  // (J^{-1} J^{-T})_ab
+          out[(o++) * stride] = f * s;
+        }
+    } else {
+      double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      if (!(det > 0.0)) atomicOr(bad, 1);
+      double Ji[2][2] = {{J[1][1] / det, -J[0][1] / det}, {-J[1][0] / det, J[0][0] / det}};
+      const double f = c * W * det;
+      out[0] = f * (Ji[0][0] * Ji[0][0] + Ji[0][1] * Ji[0][1]);
+      out[stride] = f * (Ji[0][0] * Ji[1][0] + Ji[0][1] * Ji[1][1]);
+      out[2 * stride] = f * (Ji[1][0] * Ji[1][0] + Ji[1][1] * Ji[1][1]);
+    }
+  }
+}
+
+template <int DIM>
+static cudaError_t metric_k(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s) {
+  const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
+  if (ncells == 0) return cudaSuccess;
+  const unsigned b = (unsigned)ncells;
+  switch (g.k) {
+    case 1: k_metric<DIM, 1><<<b, 128, 0, s>>>(t, g, metric, bad); break;
+    case 2: k_metric<DIM, 2><<<b, 128, 0, s>>>(t, g, metric, bad); break;
+    case 3: k_metric<DIM, 3><<<b, 128, 0, s>>>(t, g, metric, bad); break;
+    case 4: k_metric<DIM, 4><<<b, 128, 0, s>>>(t, g, metric, bad); break;
+    case 5: k_metric<DIM, 5><<<b, 256, 0, s>>>(t, g, metric, bad); break;
+    case 6: k_metric<DIM, 6><<<b, 256, 0, s>>>(t, g, metric, bad); break;
+    case 7: k_metric<DIM, 7><<<b, 256, 0, s>>>(t, g, metric, bad); break;
+    case 8: k_metric<DIM, 8><<<b, 256, 0, s>>>(t, g, metric, bad); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
+                          int64_t *launches) {
+  ++*launches;
+  return g.dim == 2 ? metric_k<2>(g, t, metric, bad, s) : metric_k<3>(g, t, metric, bad, s);
+}
+
+// ---------------------------------------------------------------------------
+// Diagonal (§8(a) a9): diag_i = sum_q sum_ab G_ab(q) dphi_i/dxhat_a dphi_i/dxhat_b,
+// by sum factorisation: for each pair (a,b) the field G_ab(q) is contracted
+// with T_d^T along each direction d, T_d = S.S (d not in {a,b}), D.S (d in
+// exactly one), D.D (d = a = b) -- elementwise products of the 1D tables.
+template <int N>
+__device__ __forceinline__ double tab(const Tables &t, int kind, int q, int i) {
+  double s = t.S[q][i], d = t.D[q][i];
+  return kind == 0 ? s * s : (kind == 1 ? d * s : d * d);
+}
+
+template <int DIM, int K, int GEOM>
+__global__ void __launch_bounds__(256) k_diagonal(const __grid_constant__ Tables t, const __grid_constant__ Geo g,
+                                                  double *__restrict__ diag, const double *__restrict__ metric,
+                                                  int cpb) {
+  constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
+  extern __shared__ double sm[];
+  const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
+  const int64_t cell0 = (int64_t)blockIdx.x * cpb;
+  const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
+  const bool active = cl < cpb;
+  double *acc = sm + cl * 2 * NV, *tmp = acc + NV;
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) sm[(idx / NV) * 2 * NV + idx % NV] = 0.0;
+  constexpr int NPAIR = DIM == 3 ? 6 : 3;
+  for (int pr = 0; pr < NPAIR; ++pr) {
+    int a, b;
+    if (DIM == 3) {
+      const int A[6] = {0, 0, 0, 1, 1, 2}, B[6] = {0, 1, 2, 1, 2, 2};
+      a = A[pr];
+      b = B[pr];
+    } else {
+      const int A[3] = {0, 0, 1}, B[3] = {0, 1, 1};
+      a = A[pr];
+      b = B[pr];
+    }
+    if (GEOM != 2 && a != b) continue;  // affine boxes: G is diagonal
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+      const int c2 = idx / NV, q = idx - c2 * NV;
+      const int64_t cell = cell0 + c2;
+      double v = 0.0;
+      if (cell < ncells) {
+        const int qd[3] = {q % N, (q / N) % N, DIM == 3 ? q / (N * N) : 0};
+        if (GEOM == 2) {
+          v = metric[(int64_t)pr * ncells * NV + cell * NV + q] * (a == b ? 1.0 : 2.0);
+        } else {
+          double W = t.w[qd[0]] * t.w[qd[1]] * (DIM == 3 ? t.w[qd[2]] : 1.0);
+          if (GEOM == 1) {
+            CellIdx ci = cell_coords(g, cell);
+            double x[3];
+            for (int d = 0; d < DIM; ++d) {
+              double cg = (double)(d == 2 ? ci.c[2] + g.cz0 : ci.c[d]);
+              x[d] = g.lo[d] + g.h[d] * (cg + t.xi[qd[d]]);
+            }
+            double vol = g.h[0] * g.h[1] * (DIM == 3 ? g.h[2] : 1.0);
+            v = W * coeff_var(x, DIM) * vol / (g.h[a] * g.h[a]);
+          } else {
+            v = W * g.fcart[a];
+          }
+        }
+      }
+      sm[c2 * 2 * NV + NV + q] = v;
+    }
+    __syncthreads();
+    for (int e = 0; e < DIM; ++e) {
+      const int kind = (e == a && e == b) ? 2 : ((e == a || e == b) ? 1 : 0);
+      if (active) {
+        double in[N], out[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) in[i] = tmp[pen_off<DIM, N>(e, p, i)];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < N; ++q) s = fma(tab<N>(t, kind, q, i), in[q], s);
+          out[i] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) tmp[pen_off<DIM, N>(e, p, i)] = out[i];
+      }
+      __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+      const int c2 = idx / NV, i = idx - c2 * NV;
+      sm[c2 * 2 * NV + i] += sm[c2 * 2 * NV + NV + i];
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int c2 = idx / NV, i = idx - c2 * NV;
+    const int64_t cell = cell0 + c2;
+    if (cell >= ncells) continue;
+    CellIdx ci = cell_coords(g, cell);
+    int64_t m[3];
+    int64_t gi = node_index<DIM, N>(g, ci, i, m);
+    if (is_constrained(g, m)) {
+      if (owner_of<DIM, N>(g, ci, i, m)) diag[gi] = 1.0;
+    } else {
+      atomicAdd(diag + gi, sm[c2 * 2 * NV + i]);
+    }
+  }
+}
+
+template <int DIM, int K, int GEOM>
+static cudaError_t diag_t(const Geo &g, const Tables &t, double *diag, const double *metric, cudaStream_t s) {
+  constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
+  int cpb = 256 / NP;
+  while (cpb > 1 && cpb * 2 * NV * 8 > 48 * 1024) --cpb;
+  if (cpb < 1) cpb = 1;
+  const int threads = ((cpb * NP + 31) / 32) * 32;
+  const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
+  const int64_t blocks = (ncells + cpb - 1) / cpb;
+  if (blocks == 0) return cudaSuccess;
+  k_diagonal<DIM, K, GEOM><<<(unsigned)blocks, threads, (size_t)cpb * 2 * NV * 8, s>>>(t, g, diag, metric, cpb);
+  return cudaGetLastError();
+}
+
+template <int DIM, int GEOM>
+static cudaError_t diag_k(const Geo &g, const Tables &t, double *diag, const double *metric, cudaStream_t s) {
+  switch (g.k) {
+    case 1: return diag_t<DIM, 1, GEOM>(g, t, diag, metric, s);
+    case 2: return diag_t<DIM, 2, GEOM>(g, t, diag, metric, s);
+    case 3: return diag_t<DIM, 3, GEOM>(g, t, diag, metric, s);
+    case 4: return diag_t<DIM, 4, GEOM>(g, t, diag, metric, s);
+    case 5: return diag_t<DIM, 5, GEOM>(g, t, diag, metric, s);
+    case 6: return diag_t<DIM, 6, GEOM>(g, t, diag, metric, s);
+    case 7: return diag_t<DIM, 7, GEOM>(g, t, diag, metric, s);
+    case 8: return diag_t<DIM, 8, GEOM>(g, t, diag, metric, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_diagonal(const Geo &g, const Tables &t, double *diag, const double *metric, cudaStream_t s,
+                            int64_t *launches) {
+  ++*launches;
+  const int gk = geom_kind(g);
+  if (g.dim == 2) {
+    if (gk == 0) return diag_k<2, 0>(g, t, diag, metric, s);
+    if (gk == 1) return diag_k<2, 1>(g, t, diag, metric, s);
+    return diag_k<2, 2>(g, t, diag, metric, s);
+  }
+  if (gk == 0) return diag_k<3, 0>(g, t, diag, metric, s);
+  if (gk == 1) return diag_k<3, 1>(g, t, diag, metric, s);
+  return diag_k<3, 2>(g, t, diag, metric, s);
+}
+
+}  // namespace mf
+
+namespace mf {
+
+// x_g = value on every constrained local DoF (R3); used for the eigenvalue
+// start vector and tests.  One pass over the local vector (setup only).
+__global__ void k_set_constrained(const __grid_constant__ Geo g, double *x, double value) {
+  const int64_t n = g.N[0] * g.N[1] * g.N[2];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m[3] = {i % g.N[0], (i / g.N[0]) % g.N[1], i / (g.N[0] * g.N[1])};
+    if (is_constrained(g, m)) x[i] = value;
+  }
+}
+
+cudaError_t launch_set_constrained(const Geo &g, double *x, double value, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  const int64_t n = g.N[0] * g.N[1] * g.N[2];
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  k_set_constrained<<<(unsigned)b, 256, 0, s>>>(g, x, value);
+  return cudaGetLastError();
+}
+
+}  // namespace mf

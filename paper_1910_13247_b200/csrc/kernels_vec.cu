@@ -1,0 +1,215 @@
+// kernels_vec.cu -- vector kernels of the solver (§8(a) a10): fills, dot
+// products (fixed block count + deterministic second pass), the CG and
+// Chebyshev recurrences of S:500-508 / S:648-656, and the plane add of the
+// halo exchange (§8(a) a8).  All FP64, grid-stride loops sized in multiples
+// of the 148 SMs.
+#include "internal.h"
+
+namespace mf {
+
+static unsigned grid_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = 148 * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+__global__ void k_zero(double *x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = 0.0;
+}
+
+cudaError_t launch_zero(double *x, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_zero<<<grid_for(n), 256, 0, s>>>(x, n);
+  return cudaGetLastError();
+}
+
+// splitmix64 of (first_global + i + 2^40 seed) -> uniform [-1,1)  (R8; same
+// counter generator as synth/, implemented here independently)
+__global__ void k_splitmix(double *x, int64_t n, int64_t first, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)(first + i) + (seed << 40) + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[i] = 2.0 * ((double)(z >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+  }
+}
+
+cudaError_t launch_splitmix(double *x, int64_t n, int64_t first_global, uint64_t seed, cudaStream_t s,
+                            int64_t *launches) {
+  ++*launches;
+  k_splitmix<<<grid_for(n), 256, 0, s>>>(x, n, first_global, seed);
+  return cudaGetLastError();
+}
+
+struct DotArgs {
+  const double *a[3];
+  const double *b[3];
+};
+
+template <int ND>
+__global__ void __launch_bounds__(256) k_dot_partial(DotArgs args, int64_t n, double *partials) {
+  double acc[ND];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) acc[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) acc[j] = fma(args.a[j][i], args.b[j][i], acc[j]);
+  }
+  __shared__ double red[ND][8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < ND; ++j) {
+    double v = acc[j];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[j][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < ND) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
+    partials[threadIdx.x * kDotBlocks + blockIdx.x] = s;
+  }
+}
+
+__global__ void k_dot_final(const double *partials, int nd, double *out) {
+  // one warp per dot, fixed order: deterministic
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j >= nd) return;
+  double s = 0.0;
+  for (int b = lane; b < kDotBlocks; b += 32) s += partials[j * kDotBlocks + b];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[j] = s;
+}
+
+cudaError_t launch_dots(int nd, const double *const *a, const double *const *b, int64_t n, double *partials,
+                        double *out, cudaStream_t s, int64_t *launches) {
+  DotArgs args{};
+  for (int j = 0; j < nd; ++j) {
+    args.a[j] = a[j];
+    args.b[j] = b[j];
+  }
+  *launches += 2;
+  if (nd == 1) k_dot_partial<1><<<kDotBlocks, 256, 0, s>>>(args, n, partials);
+  else if (nd == 2) k_dot_partial<2><<<kDotBlocks, 256, 0, s>>>(args, n, partials);
+  else k_dot_partial<3><<<kDotBlocks, 256, 0, s>>>(args, n, partials);
+  k_dot_final<<<1, 32 * nd, 0, s>>>(partials, nd, out);
+  return cudaGetLastError();
+}
+
+__global__ void k_axpby(double a, const double *__restrict__ x, double b, double *__restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a * x[i] + b * y[i];
+}
+
+cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n, cudaStream_t s,
+                         int64_t *launches) {
+  ++*launches;
+  k_axpby<<<grid_for(n), 256, 0, s>>>(a, x, b, y, n);
+  return cudaGetLastError();
+}
+
+// scal[0] = alpha: x += alpha p; r -= alpha v
+__global__ void k_cg_xr(const double *__restrict__ scal, double *__restrict__ x, double *__restrict__ r,
+                        const double *__restrict__ p, const double *__restrict__ v, int64_t n) {
+  const double alpha = scal[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    r[i] = fma(-alpha, v[i], r[i]);
+  }
+}
+
+cudaError_t launch_cg_update_xr(const double *scal, double *x, double *r, const double *p, const double *v,
+                                int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cg_xr<<<grid_for(n), 256, 0, s>>>(scal, x, r, p, v, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_cg_p(const double *__restrict__ beta, const double *__restrict__ z, double *__restrict__ p,
+                       int64_t n) {
+  const double b = beta[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], z[i]);
+}
+
+cudaError_t launch_cg_update_p(const double *beta, const double *z, double *p, int64_t n, cudaStream_t s,
+                               int64_t *launches) {
+  ++*launches;
+  k_cg_p<<<grid_for(n), 256, 0, s>>>(beta, z, p, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_cheb_init(const double *__restrict__ r, const double *__restrict__ dinv, double c0,
+                            double *__restrict__ x, double *__restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r[i] * dinv[i] * c0;
+    x[i] = v;
+    d[i] = v;
+  }
+}
+
+cudaError_t launch_cheb_init(const double *r, const double *dinv, double c0, double *x, double *d, int64_t n,
+                             cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cheb_init<<<grid_for(n), 256, 0, s>>>(r, dinv, c0, x, d, n);
+  return cudaGetLastError();
+}
+
+// d = c1 d + c2 dinv (r - ax); x += d
+__global__ void k_cheb_step(const double *__restrict__ r, const double *__restrict__ ax,
+                            const double *__restrict__ dinv, double c1, double c2, double *__restrict__ x,
+                            double *__restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double dn = c1 * d[i] + c2 * (dinv[i] * (r[i] - ax[i]));
+    d[i] = dn;
+    x[i] += dn;
+  }
+}
+
+cudaError_t launch_cheb_step(const double *r, const double *ax, const double *dinv, double c1, double c2,
+                             double *x, double *d, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cheb_step<<<grid_for(n), 256, 0, s>>>(r, ax, dinv, c1, c2, x, d, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_mul(const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ out,
+                      int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+
+cudaError_t launch_mul(const double *a, const double *b, double *out, int64_t n, cudaStream_t s,
+                       int64_t *launches) {
+  ++*launches;
+  k_mul<<<grid_for(n), 256, 0, s>>>(a, b, out, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_recip(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = 1.0 / x[i];
+}
+
+cudaError_t launch_recip(const double *x, double *y, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_recip<<<grid_for(n), 256, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_plane_add(double *__restrict__ dst, const double *__restrict__ recv, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = dst[i] + recv[i];
+}
+
+cudaError_t launch_plane_add(double *dst, const double *recv, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_plane_add<<<grid_for(n), 256, 0, s>>>(dst, recv, n);
+  return cudaGetLastError();
+}
+
+}  // namespace mf

@@ -1,0 +1,275 @@
+"""Thin Python binding of include/mf.h (ctypes).  Argument marshalling only:
+every step of the hot path runs in libmf_b200.so's CUDA kernels; PyTorch
+supplies device memory, the current CUDA stream and the process group that
+broadcasts the NCCL id.  There is no CPU fallback: if the library or a CUDA
+device is missing, constructing an Operator raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+MF_OK = 0
+STATUS = {
+    -1: "MF_ERR_ARGUMENT", -2: "MF_ERR_LENGTH", -3: "MF_ERR_SINGULAR", -4: "MF_ERR_MAX_ITERATIONS",
+    -5: "MF_ERR_BREAKDOWN", -6: "MF_ERR_CUDA", -7: "MF_ERR_NCCL", -8: "MF_ERR_OUT_OF_MEMORY",
+}
+GEOM = {"cartesian": 0, "sine": 1}
+VARIANT = {"auto": 0, "general": 1, "tile": 2}
+
+
+class MFError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+
+
+class Mesh(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("n_cells", ctypes.c_int64 * 3), ("lower", ctypes.c_double * 3),
+                ("upper", ctypes.c_double * 3), ("geometry", ctypes.c_int32), ("deform_eps", ctypes.c_double),
+                ("dirichlet_faces", ctypes.c_uint32)]
+
+
+class Coeff(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("value", ctypes.c_double)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world_size", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.POINTER(ctypes.c_uint8)), ("device", ctypes.c_int32)]
+
+
+class CGParams(ctypes.Structure):
+    _fields_ = [("rel_tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("cheb_degree", ctypes.c_int32),
+                ("cheb_range", ctypes.c_double), ("cheb_safety", ctypes.c_double), ("eig_cg_steps", ctypes.c_int32)]
+
+
+class CGResultC(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("final_rel_residual", ctypes.c_double),
+                ("lambda_max", ctypes.c_double)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("degree", ctypes.c_int32), ("geometry", ctypes.c_int32),
+                ("coeff_kind", ctypes.c_int32), ("apply_variant", ctypes.c_int32),
+                ("n_cells_local", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("bytes_algorithmic", ctypes.c_int64), ("flops_algorithmic", ctypes.c_double)]
+
+
+EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_sizes", "mf_set_stream",
+           "mf_apply", "mf_apply_host", "mf_diagonal", "mf_estimate_lambda_max", "mf_chebyshev",
+           "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing"]
+
+_lib = None
+
+
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load libmf_b200.so (built in-tree by build.py).  Loading needs no GPU."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or _build.LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing: run `python -m paper_1910_13247_b200.build` (no CPU fallback)")
+    L = ctypes.CDLL(path)
+    vp = ctypes.c_void_p
+    dp = ctypes.POINTER(ctypes.c_double)
+    i64 = ctypes.c_int64
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "mf_create": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.POINTER(Coeff), ctypes.POINTER(Dist),
+                      ctypes.POINTER(vp)],
+        "mf_sizes": [vp, i64p, i64p, i64p, i64p],
+        "mf_set_stream": [vp, vp],
+        "mf_apply": [vp, vp, i64, vp, i64],
+        "mf_apply_host": [vp, dp, i64, dp, i64],
+        "mf_diagonal": [vp, vp, i64],
+        "mf_estimate_lambda_max": [vp, ctypes.c_int32, dp],
+        "mf_chebyshev": [vp, vp, vp, i64, ctypes.c_double, ctypes.c_int32, ctypes.c_double],
+        "mf_cg_solve": [vp, vp, vp, i64, ctypes.POINTER(CGParams), ctypes.POINTER(CGResultC), dp, ctypes.c_int32],
+        "mf_get_info": [vp, ctypes.POINTER(Info)],
+        "mf_set_apply_variant": [vp, ctypes.c_int32],
+        "mf_set_kernel_timing": [vp, ctypes.c_int32],
+        "mf_kernel_timing": [vp, dp, i64p],
+        "mf_nccl_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.mf_destroy.argtypes = [vp]
+    L.mf_destroy.restype = None
+    L.mf_last_error.argtypes = []
+    L.mf_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code != MF_OK:
+        raise MFError(code, load().mf_last_error().decode())
+
+
+@dataclass
+class CGResult:
+    iterations: int
+    final_rel_residual: float
+    lambda_max: float
+    history: np.ndarray
+
+
+class Operator:
+    """v = A u for the Q_k Laplacian on a brick (see include/mf.h).
+
+    Vectors are torch.float64 CUDA tensors of length n_local (the rank's slice
+    [first_global, first_global + n_local) of the x-fastest global vector)."""
+
+    def __init__(self, n_cells, degree, dim=None, lower=None, upper=None, geometry="cartesian", eps=0.1,
+                 coeff=1.0, dirichlet_faces=None, group=None, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1910_13247_b200 needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        L = load()
+        dim = dim or len(n_cells)
+        m = Mesh()
+        m.dim = dim
+        for e in range(3):
+            m.n_cells[e] = int(n_cells[e]) if e < dim else 1
+            m.lower[e] = float(lower[e]) if lower is not None and e < dim else 0.0
+            m.upper[e] = float(upper[e]) if upper is not None and e < dim else 1.0
+        m.geometry = GEOM[geometry] if isinstance(geometry, str) else int(geometry)
+        m.deform_eps = eps
+        m.dirichlet_faces = ((1 << (2 * dim)) - 1) if dirichlet_faces is None else int(dirichlet_faces)
+        c = Coeff()
+        if isinstance(coeff, str):
+            assert coeff == "variable"
+            c.kind, c.value = 1, 0.0
+        else:
+            c.kind, c.value = 0, float(coeff)
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        dist = Dist()
+        dist.device = device
+        self._uid = None
+        if group is not None and torch.distributed.get_world_size(group) > 1:
+            import torch.distributed as tdist
+
+            rank, world = tdist.get_rank(group), tdist.get_world_size(group)
+            obj = [None]
+            if rank == 0:
+                buf = (ctypes.c_uint8 * 128)()
+                _check(L.mf_nccl_unique_id(buf))
+                obj = [bytes(buf)]
+            tdist.broadcast_object_list(obj, src=tdist.get_global_rank(group, 0), group=group)
+            self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+            dist.rank, dist.world_size = rank, world
+            dist.nccl_unique_id = ctypes.cast(self._uid, ctypes.POINTER(ctypes.c_uint8))
+        else:
+            dist.rank, dist.world_size = 0, 1
+        with torch.cuda.device(device):
+            h = ctypes.c_void_p()
+            _check(L.mf_create(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(dist), ctypes.byref(h)))
+        self._h = h
+        self.dim, self.degree, self.mesh = dim, degree, m
+        a, b, cc, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(L.mf_sizes(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(cc), ctypes.byref(d)))
+        self.n_local, self.first_global, self.n_global, self.n_owned = a.value, b.value, cc.value, d.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().mf_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # -- helpers -------------------------------------------------------------
+    def _stream(self):
+        _check(load().mf_set_stream(self._h, ctypes.c_void_p(self._torch.cuda.current_stream(self.device).cuda_stream)))
+
+    def _vec(self, x, name):
+        t = self._torch
+        if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float64 and x.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+        return ctypes.c_void_p(x.data_ptr())
+
+    def new_vector(self):
+        return self._torch.zeros(self.n_local, dtype=self._torch.float64, device=self.device)
+
+    # -- C-ABI calls ---------------------------------------------------------
+    def apply(self, src, dst=None):
+        dst = self.new_vector() if dst is None else dst
+        self._stream()
+        _check(load().mf_apply(self._h, self._vec(src, "src"), src.numel(), self._vec(dst, "dst"), dst.numel()))
+        return dst
+
+    def apply_host(self, src: np.ndarray, dst: np.ndarray | None = None) -> np.ndarray:
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        dst = np.empty_like(src) if dst is None else dst
+        dp = ctypes.POINTER(ctypes.c_double)
+        self._stream()
+        _check(load().mf_apply_host(self._h, src.ctypes.data_as(dp), src.size, dst.ctypes.data_as(dp), dst.size))
+        return dst
+
+    def apply_host_ptr(self, src_ptr: int, dst_ptr: int):
+        """mf_apply_host on raw host pointers (e.g. pinned torch tensors)."""
+        dp = ctypes.POINTER(ctypes.c_double)
+        self._stream()
+        _check(load().mf_apply_host(self._h, ctypes.cast(src_ptr, dp), self.n_local, ctypes.cast(dst_ptr, dp),
+                                    self.n_local))
+
+    def diagonal(self, out=None):
+        out = self.new_vector() if out is None else out
+        self._stream()
+        _check(load().mf_diagonal(self._h, self._vec(out, "diag"), out.numel()))
+        return out
+
+    def estimate_lambda_max(self, steps: int = 12) -> float:
+        lam = ctypes.c_double()
+        self._stream()
+        _check(load().mf_estimate_lambda_max(self._h, steps, ctypes.byref(lam)))
+        return lam.value
+
+    def chebyshev(self, r, lam: float, degree: int = 6, smoothing_range: float = 20.0, out=None):
+        out = self.new_vector() if out is None else out
+        self._stream()
+        _check(load().mf_chebyshev(self._h, self._vec(r, "r"), self._vec(out, "z"), r.numel(), lam, degree,
+                                   smoothing_range))
+        return out
+
+    def cg_solve(self, b, x=None, rel_tol=1e-10, max_iter=10000, cheb_degree=6, cheb_range=20.0,
+                 cheb_safety=1.2, eig_cg_steps=12, history_cap=20000):
+        x = self.new_vector() if x is None else x
+        p = CGParams(rel_tol, max_iter, cheb_degree, cheb_range, cheb_safety, eig_cg_steps)
+        r = CGResultC()
+        hist = np.zeros(history_cap)
+        self._stream()
+        code = load().mf_cg_solve(self._h, self._vec(b, "b"), self._vec(x, "x"), b.numel(), ctypes.byref(p),
+                                  ctypes.byref(r), hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), history_cap)
+        _check(code)
+        return x, CGResult(r.iterations, r.final_rel_residual, r.lambda_max, hist[:r.iterations].copy())
+
+    def info(self) -> dict:
+        i = Info()
+        _check(load().mf_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in Info._fields_}
+
+    def set_variant(self, variant):
+        v = VARIANT[variant] if isinstance(variant, str) else int(variant)
+        _check(load().mf_set_apply_variant(self._h, v))
+
+    def kernel_timing(self, enable: bool):
+        _check(load().mf_set_kernel_timing(self._h, 1 if enable else 0))
+
+    def kernel_time(self):
+        """(summed ms, launches) of the dominant apply kernel since kernel_timing(True)."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        _check(load().mf_kernel_timing(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
