@@ -284,7 +284,7 @@ static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
 extern "C" mf_status mf_set_kernel_timing(mf_op *op, int32_t enable) {
   if (!op) return fail(MF_ERR_ARGUMENT, "null op");
   op->timing = enable != 0;
-  op->ev_used = 0;
+  if (op->timing) op->ev_used = 0;  // a new window; disabling keeps the events for mf_kernel_timing
   return MF_OK;
 }
 

@@ -97,7 +97,9 @@ def test_cg_iteration_counts_match_oracle(case, rhs, tol, torch):
     else:
         n = min(len(ref.history), res.iterations)
         np.testing.assert_allclose(res.history[:n], ref.history[:n], rtol=1e-8)
-    np.testing.assert_allclose(res.history, ref.history[:res.iterations], rtol=1e-6)
+    # histories agree to 1e-6 relative above the round-off floor of the recursive
+    # residual (|r| is only known to ~eps * cond(A) |b|; 1e-13 |b| covers cond <= 1e3)
+    np.testing.assert_allclose(res.history, ref.history[:res.iterations], rtol=1e-6, atol=1e-13 * normb)
     assert rel_l2(x, ref.x) <= 1e-8
     assert res.final_rel_residual <= tol
 
