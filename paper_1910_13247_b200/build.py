@@ -36,18 +36,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every csrc/ source with nvcc for sm_100a and link LIB (or `out`)."""
+    lib_path = out or LIB
+    if not force and not defines and not needs_build():
         return LIB
     inc, lib = nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.lower() for d in defines))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc,
-               "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-c", src, "-o", obj]
+               "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", *[f"-D{d}" for d in defines],
+               "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = []
         if verbose:
@@ -57,10 +60,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for p, cmd in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", lib, "-l:libnccl.so.2",
+    link = [NVCC, *ARCH, "-shared", "-o", lib_path, *objs, "-L", lib, "-l:libnccl.so.2",
             f"-Xlinker=-rpath={lib}", "-lcudart"]
     subprocess.check_call(link)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

@@ -71,6 +71,34 @@ def test_apply_matches_assembled_oracle(case, torch):
     np.testing.assert_array_equal(y[m], x[m])
 
 
+TILE_CASES = [
+    dict(dim=3, n_cells=(9, 10, 11), k=2),                       # 2x2 ragged tiles, many z-chunks
+    dict(dim=3, n_cells=(16, 16, 16), k=2, dirichlet=0),
+    dict(dim=3, n_cells=(9, 9, 13), k=3, upper=(1.0, 2.0, 0.5), coeff=3.0),
+    dict(dim=3, n_cells=(9, 17, 7), k=4),                        # 3x3 tiles, ragged in x and y
+    dict(dim=3, n_cells=(4, 8, 5), k=4, dirichlet=0b011001),
+    dict(dim=3, n_cells=(1, 1, 1), k=4),
+    dict(dim=3, n_cells=(5, 3, 20), k=4, dirichlet=0),
+]
+
+
+@pytest.mark.parametrize("variant", ["general", "tile"])
+@pytest.mark.parametrize("case", TILE_CASES, ids=_id)
+def test_cartesian_variants_match_oracle(case, variant, torch):
+    p = oracle_problem(case)
+    A = oracle.CSR(p)
+    op = cuda_operator(case)
+    op.set_variant(variant)
+    assert op.info()["apply_variant"] == {"general": 1, "tile": 2}[variant]
+    for s in (1, 2, 3):
+        x = seeded(A.n, s)
+        y_ref = A @ x
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_l2(y, y_ref) <= CUDA_ORACLE_TOL, (s, rel_l2(y, y_ref))
+    m = oracle.constrained_mask_fast(p)
+    np.testing.assert_array_equal(y[m], x[m])
+
+
 @pytest.mark.parametrize("case", CASES[::2], ids=_id)
 def test_diagonal_matches_assembled_oracle(case, torch):
     p = oracle_problem(case)

@@ -1,0 +1,28 @@
+"""Small driver for ncu captures: build one operator and run a few applies.
+python tools/prof_apply.py [--config cfg3] [--variant auto] [--reps 5]"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from bench import CONFIGS  # noqa: E402
+from paper_1910_13247_b200 import Operator  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg3")
+ap.add_argument("--variant", default="auto")
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+nc, k, geom, coeff, _ = CONFIGS[a.config]
+op = Operator(nc, k, geometry=geom, coeff=coeff)
+op.set_variant(a.variant)
+x = torch.from_numpy(synth.vector(op.n_local, 0)).cuda()
+y = torch.empty_like(x)
+for _ in range(a.reps):
+    op.apply(x, y)
+torch.cuda.synchronize()
+print("ok", op.info())
