@@ -90,6 +90,17 @@ const char *mf_last_error(void);
 /* NCCL unique id (128 bytes) for mf_dist, created on rank 0 and broadcast by the caller. */
 mf_status mf_nccl_unique_id(uint8_t *out128);
 
+/* The z-slab partition mf_create uses for (rank, world_size), computed on the
+ * host without a GPU: rank r owns cell layers [cz0, cz1) =
+ * [r nz / P, (r+1) nz / P); its local vector is the global slice
+ * [first_global, first_global + n_local) = DoF planes k cz0 .. k cz1 inclusive;
+ * the first n_owned entries are owned (the shared upper plane belongs to the
+ * upper rank); plane = Nx Ny doubles is the size of one halo message.
+ * MF_ERR_ARGUMENT for an invalid mesh/degree or nz < world_size. */
+mf_status mf_partition(const mf_mesh *mesh, int32_t degree, int32_t rank, int32_t world_size,
+                       int64_t *cz0, int64_t *cz1, int64_t *first_global, int64_t *n_local,
+                       int64_t *n_owned, int64_t *plane);
+
 /* Local / global sizes (see Conventions). */
 mf_status mf_sizes(const mf_op *op, int64_t *n_local, int64_t *first_global,
                    int64_t *n_global, int64_t *n_owned);

@@ -82,16 +82,43 @@ static int64_t ipow(int64_t b, int e) {
 }
 static int64_t ncells_local(const Geo &g) { return g.nc[0] * g.nc[1] * (g.dim == 3 ? g.nc[2] : 1); }
 
-extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff, const mf_dist *dist,
-                               mf_op **out) {
-  if (!mesh || !coeff || !out) return fail(MF_ERR_ARGUMENT, "null argument");
-  *out = nullptr;
+static mf_status check_mesh(const mf_mesh *mesh, int32_t degree) {
+  if (!mesh) return fail(MF_ERR_ARGUMENT, "null mesh");
   if (mesh->dim != 2 && mesh->dim != 3) return fail(MF_ERR_ARGUMENT, "dim must be 2 or 3");
   if (degree < 1 || degree > 8) return fail(MF_ERR_ARGUMENT, "degree must be in 1..8");
   for (int e = 0; e < mesh->dim; ++e) {
     if (mesh->n_cells[e] < 1) return fail(MF_ERR_ARGUMENT, "n_cells must be >= 1");
     if (!(mesh->lower[e] < mesh->upper[e])) return fail(MF_ERR_ARGUMENT, "lower must be < upper");
   }
+  return MF_OK;
+}
+
+extern "C" mf_status mf_partition(const mf_mesh *mesh, int32_t degree, int32_t rank, int32_t world,
+                                  int64_t *cz0, int64_t *cz1, int64_t *first_global, int64_t *n_local,
+                                  int64_t *n_owned, int64_t *plane) {
+  STATUS_TRY(check_mesh(mesh, degree));
+  if (world < 1 || rank < 0 || rank >= world) return fail(MF_ERR_ARGUMENT, "bad rank/world_size");
+  const bool d3 = mesh->dim == 3;
+  const int64_t nz = d3 ? mesh->n_cells[2] : 1;
+  if (world > 1 && (!d3 || nz < world)) return fail(MF_ERR_ARGUMENT, "z-slabs need dim 3 and nz >= world_size");
+  const int64_t Nx = (int64_t)degree * mesh->n_cells[0] + 1, Ny = (int64_t)degree * mesh->n_cells[1] + 1;
+  const int64_t a = d3 ? (int64_t)rank * nz / world : 0, b = d3 ? (int64_t)(rank + 1) * nz / world : 1;
+  const int64_t pl = Nx * Ny;
+  const int64_t nl = d3 ? pl * ((int64_t)degree * (b - a) + 1) : pl;
+  if (cz0) *cz0 = a;
+  if (cz1) *cz1 = b;
+  if (first_global) *first_global = d3 ? (int64_t)degree * a * pl : 0;
+  if (n_local) *n_local = nl;
+  if (n_owned) *n_owned = (world > 1 && rank < world - 1) ? nl - pl : nl;
+  if (plane) *plane = pl;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff, const mf_dist *dist,
+                               mf_op **out) {
+  if (!mesh || !coeff || !out) return fail(MF_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  STATUS_TRY(check_mesh(mesh, degree));
   if (mesh->geometry != MF_GEOM_CARTESIAN && mesh->geometry != MF_GEOM_SINE)
     return fail(MF_ERR_ARGUMENT, "unknown geometry");
   if (coeff->kind != MF_COEFF_CONSTANT && coeff->kind != MF_COEFF_VARIABLE)
@@ -126,9 +153,16 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
     g.h[e] = (g.hi[e] - g.lo[e]) / (double)g.nc[e];
   }
   g.ncz_global = g.nc[2];
-  // z-slab of whole cell layers: rank r gets [r nz / P, (r+1) nz / P)
-  const int64_t cz0 = g.dim == 3 ? (int64_t)rank * g.nc[2] / world : 0;
-  const int64_t cz1 = g.dim == 3 ? (int64_t)(rank + 1) * g.nc[2] / world : 1;
+  // z-slab of whole cell layers (mf_partition is the single source of the arithmetic)
+  int64_t cz0 = 0, cz1 = 1;
+  {
+    mf_status ps = mf_partition(mesh, degree, rank, world, &cz0, &cz1, &op->first_global, &op->n_local,
+                                &op->n_owned, &op->plane);
+    if (ps != MF_OK) {
+      delete op;
+      return ps;
+    }
+  }
   g.cz0 = cz0;
   if (g.dim == 3) g.nc[2] = cz1 - cz0;
   for (int e = 0; e < 3; ++e) g.N[e] = e < g.dim ? (int64_t)degree * g.nc[e] + 1 : 1;
@@ -146,11 +180,7 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
   for (int e = 0; e < g.dim; ++e) g.fcart[e] = coeff->value * vol / (g.h[e] * g.h[e]);
   build_tables(degree, &op->t);
 
-  op->plane = g.N[0] * g.N[1];
-  op->n_local = g.N[0] * g.N[1] * g.N[2];
-  op->first_global = g.dim == 3 ? (int64_t)degree * cz0 * op->plane : 0;
   op->n_global = g.dim == 3 ? op->plane * ((int64_t)degree * g.ncz_global + 1) : op->n_local;
-  op->n_owned = (world > 1 && rank < world - 1) ? op->n_local - op->plane : op->n_local;
 
   auto cleanup = [&](mf_status s) {
     mf_destroy(op);

@@ -63,7 +63,8 @@ class Info(ctypes.Structure):
 
 EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_sizes", "mf_set_stream",
            "mf_apply", "mf_apply_host", "mf_diagonal", "mf_estimate_lambda_max", "mf_chebyshev",
-           "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing"]
+           "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing",
+           "mf_partition"]
 
 _lib = None
 
@@ -97,6 +98,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "mf_set_kernel_timing": [vp, ctypes.c_int32],
         "mf_kernel_timing": [vp, dp, i64p],
         "mf_nccl_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
+        "mf_partition": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                         i64p, i64p, i64p, i64p, i64p, i64p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -113,6 +116,29 @@ def load(path: str | None = None) -> ctypes.CDLL:
 def _check(code: int):
     if code != MF_OK:
         raise MFError(code, load().mf_last_error().decode())
+
+
+def make_mesh(n_cells, dim=None, lower=None, upper=None, geometry="cartesian", eps=0.1, dirichlet_faces=None):
+    dim = dim or len(n_cells)
+    m = Mesh()
+    m.dim = dim
+    for e in range(3):
+        m.n_cells[e] = int(n_cells[e]) if e < dim else 1
+        m.lower[e] = float(lower[e]) if lower is not None and e < dim else 0.0
+        m.upper[e] = float(upper[e]) if upper is not None and e < dim else 1.0
+    m.geometry = GEOM[geometry] if isinstance(geometry, str) else int(geometry)
+    m.deform_eps = eps
+    m.dirichlet_faces = ((1 << (2 * dim)) - 1) if dirichlet_faces is None else int(dirichlet_faces)
+    return m
+
+
+def partition(n_cells, degree, rank, world_size, **mesh_kw) -> dict:
+    """mf_partition: the z-slab of `rank` (host arithmetic only, no GPU needed)."""
+    m = make_mesh(n_cells, **mesh_kw)
+    vals = [ctypes.c_int64() for _ in range(6)]
+    _check(load().mf_partition(ctypes.byref(m), degree, rank, world_size, *[ctypes.byref(v) for v in vals]))
+    keys = ["cz0", "cz1", "first_global", "n_local", "n_owned", "plane"]
+    return {k: v.value for k, v in zip(keys, vals)}
 
 
 @dataclass
