@@ -251,14 +251,15 @@ extern "C" mf_status mf_set_stream(mf_op *op, void *s) {
 
 static int chosen_variant(const mf_op *op) {
   if (op->variant != kVariantAuto) return op->variant;
-  return cart_tile_supported(op->g) ? kVariantCartTile : kVariantGeneral;
+  return cart_plane_supported(op->g) ? kVariantCartPlane : kVariantGeneral;
 }
 
 extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
   if (!op) return fail(MF_ERR_ARGUMENT, "null op");
-  if (variant == kVariantCartTile && !cart_tile_supported(op->g))
-    return fail(MF_ERR_ARGUMENT, "tile kernel needs dim 3, Cartesian geometry, constant coefficient");
-  if (variant < 0 || variant > kVariantCartTile) return fail(MF_ERR_ARGUMENT, "unknown variant");
+  if ((variant == kVariantCartTile && !cart_tile_supported(op->g)) ||
+      (variant == kVariantCartPlane && !cart_plane_supported(op->g)))
+    return fail(MF_ERR_ARGUMENT, "tile/plane kernels need dim 3, Cartesian geometry, constant coefficient, k 2..4");
+  if (variant < 0 || variant > kVariantCartPlane) return fail(MF_ERR_ARGUMENT, "unknown variant");
   op->variant = variant;
   return MF_OK;
 }
@@ -301,6 +302,10 @@ static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
   if (var == kVariantCartTile) {
     STATUS_TRY(timing_mark(op));
     CUDA_TRY(launch_apply_cart_tile(op->g, op->t, src, dst, op->stream, &op->launches));
+    STATUS_TRY(timing_mark(op));
+  } else if (var == kVariantCartPlane) {
+    STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches));
     STATUS_TRY(timing_mark(op));
   } else {
     CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));

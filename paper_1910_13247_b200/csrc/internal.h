@@ -49,7 +49,8 @@ struct Geo {
 enum Variant {
   kVariantAuto = 0,
   kVariantGeneral = 1,  // 12-sweep collocation kernel, any dim/k/geometry
-  kVariantCartTile = 2, // Cartesian constant-coefficient 3D tile kernel
+  kVariantCartTile = 2, // Cartesian constant-coefficient 3D tile kernel (slab form)
+  kVariantCartPlane = 3, // Cartesian constant-coefficient 3D, 2D-first / z-last form
 };
 
 // Kernel launchers (return cudaError_t of the launch).
@@ -58,6 +59,9 @@ cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *sr
 cudaError_t launch_apply_cart_tile(const Geo &g, const Tables &t, const double *src, double *dst,
                                    cudaStream_t s, int64_t *launches);
 bool cart_tile_supported(const Geo &g);
+cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst,
+                                    cudaStream_t s, int64_t *launches);
+bool cart_plane_supported(const Geo &g);
 cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
                           int64_t *launches);
 cudaError_t launch_diagonal(const Geo &g, const Tables &t, double *diag, const double *metric,

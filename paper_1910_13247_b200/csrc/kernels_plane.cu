@@ -1,0 +1,398 @@
+// kernels_plane.cu -- Cartesian, constant-coefficient 3D apply in "2D first, z last"
+// form (apply variant 3, the default for k = 2..4).
+//
+// The cell operator of the affine box cell is the Gauss(k+1)-exact Kronecker form
+// (see kernels_tile.cu)
+//     A_c = [Kx' (x) My + Mx (x) Ky'] (x) Mz  +  [Mx (x) My] (x) Kz'     (x, y | z)
+// so with the x-y operators applied on every DoF plane p and summed over the
+// cells that share a node in x-y,
+//     P_p = sum_{cells} (Kx' (x) M + M (x) Ky') u_p,      Q_p = sum_{cells} (M (x) M) u_p,
+// the result is a 1D operator in z per node column:
+//     v = sum_{z-cells} (Mz P + Kz' Q).
+// P and Q are computed ONCE per DoF plane (k planes per cell layer instead of
+// the k+1 z-levels of the slab form), the z-sweep runs in registers of one
+// thread per node column, and nothing but u, P and Q goes through shared
+// memory: ~40 FP64 instructions and ~8 shared-memory accesses per DoF.
+//
+// Per thread block: a tile of TX x TY cells marching through a z-chunk of cell
+// layers (persistent blocks walk (tile, chunk) items).  Per layer:
+//   face phase    thread per (cell, plane p = 1..k): u_p on the cell face from the
+//                 cp.async stage, y sweeps column by column, x sweeps row by row,
+//                 even-odd; P and Q of the face written to shared memory;
+//   column phase  thread per (cell, row j): the k node columns (i = 0..k-1, j) the
+//                 cell owns -- the gather of P and Q from the own / left / lower /
+//                 diagonal face is compile-time in i -- plus one of the tile's
+//                 right-edge / top-edge columns; prefetch of the next layer
+//                 (cp.async), z-sweep in even-odd form with the plane-0 values
+//                 carried from the previous layer, store the k finished planes.
+// Shared tile-edge / chunk-plane nodes: init kernel + FP64 atomics (tile_common.cuh).
+#include "tile_common.cuh"
+
+namespace mf {
+
+template <int K, int TX, int TY>
+struct PlaneShape {
+  static constexpr int N = K + 1;
+  static constexpr int NXc = K * TX + 1, NYc = K * TY + 1, NCOL = NXc * NYc;
+  static constexpr int NCELL = TX * TY;
+  static constexpr int NT = NCELL * K;          // face phase: (cell, p = 1..K); column phase: (cell, j)
+  static_assert(NT % 32 == 0, "tile must give whole warps");
+  static_assert(NXc + NYc - 1 <= NT, "one edge column per thread");
+  static constexpr int SPL = NCOL | 1;          // stage plane pitch
+  static constexpr int STG = N * SPL;           // u on planes 0..K of a layer
+  static constexpr int FACE = N * N;
+  static constexpr int NV = NCELL * N * FACE;   // P (or Q): faces of planes 0..K
+  static constexpr size_t SMEM = sizeof(double) * (STG + 2 * NV);
+};
+
+template <int K, int TX, int TY, bool ISO>
+__global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
+    k_apply_plane(const __grid_constant__ TileParams P, const double *__restrict__ src, double *__restrict__ dst) {
+  using S = PlaneShape<K, TX, TY>;
+  constexpr int N = S::N, NXc = S::NXc, NCELL = S::NCELL, SPL = S::SPL, FACE = S::FACE;
+  constexpr int h = (N + 1) / 2;
+  constexpr int PSTRIDE = TX * FACE;       // face slot of (cx, cy, p) = cx + TX (p + N cy)
+  constexpr int YSTRIDE = TX * N * FACE;   // cy -> cy + 1
+  extern __shared__ double sm[];
+  double *Us = sm, *Vp = sm + S::STG, *Vq = Vp + S::NV;
+
+  const int ntile = P.ntx * P.nty, nitems = ntile * P.nch;
+  const int Nx = (int)P.Nx, Ny = (int)P.Ny;
+  const int64_t plane = P.Nx * P.Ny;
+  const uint32_t d = P.dirichlet;
+  const int tid = threadIdx.x;
+  const bool z_lo_c = (d & 16u) != 0, z_hi_c = (d & 32u) != 0;
+  // face phase: (x-cell fastest, then plane, then y-cell)
+  const int fcx = tid % TX, fp = 1 + (tid / TX) % K, fcy = tid / (TX * K);
+  // column phase: cell c = (ccx, ccy) and row jr of its owned columns
+  const int cc = tid % NCELL, jr = tid / NCELL, ccx = cc % TX, ccy = cc / TX;
+
+  struct Item {
+    int tx, ty, chunk, cx0, cy0, nvx, nvy, cz_begin, cz_end;
+    int64_t base0;
+  };
+  auto item_of = [&](int it) {
+    Item I;
+    const int tile = it % ntile;
+    I.chunk = it / ntile;
+    I.tx = tile % P.ntx;
+    I.ty = tile / P.ntx;
+    I.cx0 = TX * I.tx;
+    I.cy0 = TY * I.ty;
+    I.nvx = min(TX, P.ncx - I.cx0);
+    I.nvy = min(TY, P.ncy - I.cy0);
+    I.cz_begin = I.chunk * P.LZ;
+    I.cz_end = min(I.cz_begin + P.LZ, P.ncz);
+    I.base0 = (int64_t)K * I.cz_begin * plane + (int64_t)K * I.cy0 * P.Nx + (int64_t)K * I.cx0;
+    return I;
+  };
+  // this thread's edge column of an item: tile right edge x = K nvx (e <= K nvy),
+  // then the top edge y = K nvy (x < K nvx); -1 if none
+  auto edge_xy = [&](const Item &I, int &x, int &y) {
+    const int nr = K * I.nvy + 1, ne = nr + K * I.nvx;
+    if (tid >= ne) return false;
+    if (tid < nr) {
+      x = K * I.nvx;
+      y = tid;
+    } else {
+      x = tid - nr;
+      y = K * I.nvy;
+    }
+    return true;
+  };
+  auto xy_cons = [&](const Item &I, int x, int y) {
+    const int gx = K * I.cx0 + x, gy = K * I.cy0 + y;
+    return ((d & 1u) && gx == 0) || ((d & 2u) && gx == Nx - 1) || ((d & 4u) && gy == 0) ||
+           ((d & 8u) && gy == Ny - 1);
+  };
+
+  // cp.async of node planes l0..K of layer cz of item I (this thread's columns) into the stage
+  auto prefetch = [&](const Item &I, int cz, int l0) {
+    const double *sp0 = src + I.base0 + (int64_t)K * (cz - I.cz_begin) * plane;
+    const int64_t gzb = (int64_t)K * cz;
+    const bool own_ok = ccx < I.nvx && ccy < I.nvy;
+    const int y = K * ccy + jr;
+    const bool ycons = (d & 4u) && K * I.cy0 + y == 0;
+    const bool xcons0 = (d & 1u) && K * (I.cx0 + ccx) == 0;  // the cell's i = 0 column on the x- face
+    int ex = 0, ey = 0;
+    const bool has_e = edge_xy(I, ex, ey);
+    const bool e_ok = has_e && !xy_cons(I, ex, ey);
+#pragma unroll
+    for (int l = 0; l <= K; ++l) {
+      if (l < l0) continue;
+      const bool zc = (z_lo_c && gzb + l == 0) || (z_hi_c && gzb + l == P.Nz - 1);
+      const double *spl = sp0 + l * plane;
+      double *ul = Us + l * SPL;
+      if (own_ok) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const bool ok = !zc && !ycons && !(i == 0 && xcons0);
+          cp_async8z(ul + y * NXc + K * ccx + i, ok ? spl + y * Nx + K * ccx + i : src, ok ? 8u : 0u);
+        }
+      }
+      if (has_e) {
+        const bool ok = e_ok && !zc;
+        cp_async8z(ul + ey * NXc + ex, ok ? spl + ey * Nx + ex : src, ok ? 8u : 0u);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  // ---- face: P and Q on the face of cell (fcx, fcy) at plane p from u on that plane
+  auto face = [&](int p) {
+    const double *Ul = Us + p * SPL + (K * fcy) * NXc + K * fcx;
+    double *Pf = Vp + (fcx + TX * (p + N * fcy)) * FACE, *Qf = Vq + (fcx + TX * (p + N * fcy)) * FACE;
+    double c[N][N], g[N][N];  // [j][i]: c = M_y u, g = Ky' u
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double uv[N], e[h], o[h], ve[h], vo[h], t[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) uv[j] = Ul[j * NXc + i];
+      eo_split<N>(uv, e, o);
+      eo_first<N>(P.M, e, o, ve, vo);
+      eo_combine<N>(ve, vo, t);
+#pragma unroll
+      for (int j = 0; j < N; ++j) c[j][i] = t[j];
+      if (!ISO) {
+#pragma unroll
+        for (int q = 0; q < h; ++q) {
+          e[q] *= P.ry;
+          o[q] *= P.ry;
+        }
+      }
+      eo_first<N>(P.K, e, o, ve, vo);
+      eo_combine<N>(ve, vo, t);
+#pragma unroll
+      for (int j = 0; j < N; ++j) g[j][i] = t[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double ec[h], oc[h], eg[h], og[h], ve[h], vo[h], t[N];
+      eo_split<N>(c[j], ec, oc);
+      eo_split<N>(g[j], eg, og);
+      eo_first<N>(P.K, ec, oc, ve, vo);  // P = Kx' c + Mx g
+      eo_acc<N>(P.M, eg, og, ve, vo);
+      eo_combine<N>(ve, vo, t);
+#pragma unroll
+      for (int i = 0; i < N; ++i) Pf[j * N + i] = t[i];
+      eo_first<N>(P.M, ec, oc, ve, vo);  // Q = Mx c
+      eo_combine<N>(ve, vo, t);
+#pragma unroll
+      for (int i = 0; i < N; ++i) Qf[j * N + i] = t[i];
+    }
+  };
+
+  // ---- z-sweep of one column: v = Mz P + Kz' Q (even-odd), carries, stores
+  auto zcolumn = [&](const double *pb, const double *qb, double &vcar, bool first, bool last, bool cons, bool shared,
+                     double *out, int64_t gzb, int chunk) {
+    double e[h], o[h], ve[h], vo[h], v[N];
+    eo_split<N>(pb, e, o);
+    eo_first<N>(P.M, e, o, ve, vo);
+    eo_split<N>(qb, e, o);
+    if (!ISO) {
+#pragma unroll
+      for (int q = 0; q < h; ++q) {
+        e[q] *= P.rz;
+        o[q] *= P.rz;
+      }
+    }
+    eo_acc<N>(P.K, e, o, ve, vo);
+    eo_combine<N>(ve, vo, v);
+    if (!first) v[0] += vcar;
+    vcar = v[K];
+    if (cons) return;
+#pragma unroll
+    for (int l = 0; l <= K; ++l) {
+      if (l == K && !last) break;  // carried to the next layer
+      const int64_t gz = gzb + l;
+      if ((z_lo_c && gz == 0) || (z_hi_c && gz == P.Nz - 1)) continue;
+      const bool at = shared || (l == 0 && first && chunk > 0) || (l == K && chunk < P.nch - 1);
+      double *p = out + l * plane;
+      if (at) atomicAdd(p, v[l]);
+      else *p = v[l];
+    }
+  };
+
+  int item = blockIdx.x;
+  if (item >= nitems) return;
+  Item G = item_of(item);
+  prefetch(G, G.cz_begin, 0);
+  double pcar[K + 1], qcar[K + 1], vcar[K + 1];  // owned columns i = 0..K-1, [K] = edge column
+
+  while (true) {
+    const int cz_begin = G.cz_begin, cz_end = G.cz_end, chunk = G.chunk;
+    const int64_t base0 = G.base0;
+    const int next = item + gridDim.x;
+    const bool face_ok = fcx < G.nvx && fcy < G.nvy;
+    // owned columns (i, jr) of cell (ccx, ccy)
+    const bool own_ok = ccx < G.nvx && ccy < G.nvy;
+    const bool hasL = ccx > 0, hasB = ccy > 0 && jr == 0;
+    const int yown = K * ccy + jr;
+    const bool ycons = (d & 4u) && K * G.cy0 + yown == 0;
+    const bool xcons0 = (d & 1u) && K * (G.cx0 + ccx) == 0;
+    const bool shx0 = ccx == 0 && G.tx > 0, shy = jr == 0 && ccy == 0 && G.ty > 0;
+    const int own0 = (ccx + YSTRIDE / FACE * ccy) * FACE + jr * N;  // face offset of (i = 0, jr), plane 0
+    // the edge column: faces of the tile containing it
+    int ex = 0, ey = 0;
+    const bool has_e = edge_xy(G, ex, ey);
+    bool e_cons = false, e_sh = false;
+    int eo[4] = {-1, -1, -1, -1};
+    if (has_e) {
+      e_cons = xy_cons(G, ex, ey);
+      const int gx = K * G.cx0 + ex, gy = K * G.cy0 + ey;
+      e_sh = (ex == 0 && G.tx > 0) || (ex == K * G.nvx && gx < Nx - 1) || (ey == 0 && G.ty > 0) ||
+             (ey == K * G.nvy && gy < Ny - 1);
+      const int cxa = ex / K - (ex % K == 0 ? 1 : 0), cxb = min(ex / K, G.nvx - 1);
+      const int cya = ey / K - (ey % K == 0 ? 1 : 0), cyb = min(ey / K, G.nvy - 1);
+      int n = 0;
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int cx = a == 0 ? cxa : cxb, cy = b == 0 ? cya : cyb;
+          const bool ok = cx >= 0 && cy >= 0 && (a == 0 || cxb != cxa) && (b == 0 || cyb != cya);
+          if (ok) {
+            const int o = (cx + TX * N * cy) * FACE + (ey - K * cy) * N + (ex - K * cx);
+            if (n == 0) eo[0] = o;
+            else if (n == 1) eo[1] = o;
+            else if (n == 2) eo[2] = o;
+            else eo[3] = o;
+            ++n;
+          }
+        }
+    }
+
+    for (int cz = cz_begin; cz < cz_end; ++cz) {
+      const bool first = cz == cz_begin, last = cz + 1 == cz_end;
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      // ---- face phase
+      if (face_ok) {
+        face(fp);
+        if (first && fp == 1) face(0);  // the chunk's bottom plane (once per item)
+      }
+      __syncthreads();
+      // ---- column phase: prefetch the next layer, then gather P, Q and sweep in z
+      if (!last) {
+        prefetch(G, cz + 1, 1);
+      } else if (next < nitems) {
+        prefetch(item_of(next), item_of(next).cz_begin, 0);
+      }
+      const int64_t gzb = (int64_t)K * cz;
+      double *outl = dst + base0 + (int64_t)K * (cz - cz_begin) * plane;
+      if (own_ok) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          double pb[N], qb[N];
+#pragma unroll
+          for (int p = 0; p < N; ++p) {
+            if (p == 0 && !first) {
+              pb[0] = pcar[i];
+              qb[0] = qcar[i];
+              continue;
+            }
+            const int o = own0 + p * PSTRIDE + i;
+            double sp_ = Vp[o], sq_ = Vq[o];
+            if (i == 0 && hasL) {  // left face, its local (K, jr)
+              sp_ += Vp[o - FACE + K];
+              sq_ += Vq[o - FACE + K];
+            }
+            if (hasB) {  // lower face, its local (i, K)
+              sp_ += Vp[o - YSTRIDE + K * N];
+              sq_ += Vq[o - YSTRIDE + K * N];
+              if (i == 0 && hasL) {  // diagonal face, its local (K, K)
+                sp_ += Vp[o - YSTRIDE - FACE + K * N + K];
+                sq_ += Vq[o - YSTRIDE - FACE + K * N + K];
+              }
+            }
+            pb[p] = sp_;
+            qb[p] = sq_;
+          }
+          pcar[i] = pb[K];
+          qcar[i] = qb[K];
+          const bool cons = ycons || (i == 0 && xcons0), shared = shy || (i == 0 && shx0);
+          zcolumn(pb, qb, vcar[i], first, last, cons, shared, outl + yown * Nx + K * ccx + i, gzb, chunk);
+        }
+      }
+      if (has_e) {
+        double pb[N], qb[N];
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+          if (p == 0 && !first) {
+            pb[0] = pcar[K];
+            qb[0] = qcar[K];
+            continue;
+          }
+          double sp_ = 0.0, sq_ = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (eo[q] >= 0) {
+              sp_ += Vp[eo[q] + p * PSTRIDE];
+              sq_ += Vq[eo[q] + p * PSTRIDE];
+            }
+          pb[p] = sp_;
+          qb[p] = sq_;
+        }
+        pcar[K] = pb[K];
+        qcar[K] = qb[K];
+        zcolumn(pb, qb, vcar[K], first, last, e_cons, e_sh, outl + ey * Nx + ex, gzb, chunk);
+      }
+    }
+    if (next >= nitems) break;
+    item = next;
+    G = item_of(item);
+  }
+}
+
+template <int K, int TX, int TY, bool ISO>
+static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+                                  int64_t *launches) {
+  using S = PlaneShape<K, TX, TY>;
+  TileParams P;
+  tile_params_common(g, t, TX, TY, &P);
+  static int occ = 0, sms = 0;
+  if (occ == 0) {
+    cudaFuncSetAttribute(k_apply_plane<K, TX, TY, ISO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_plane<K, TX, TY, ISO>, S::NT, S::SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ < 1) occ = 1;
+    if (sms < 1) sms = 148;
+  }
+  const int slots = sms * occ;
+  tile_choose_chunks(&P, slots, 1.0 / K + 0.25);  // the bottom plane costs one extra face per cell
+  cudaError_t e = tile_launch_init(P, g, K, TX, TY, src, dst, s, launches);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  const int items = P.ntx * P.nty * P.nch;
+  const int blocks = std::min(items, slots);
+  k_apply_plane<K, TX, TY, ISO><<<blocks, S::NT, S::SMEM, s>>>(P, src, dst);
+  return cudaGetLastError();
+}
+
+bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }
+
+cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+                                    int64_t *launches) {
+  const bool iso = g.fcart[0] == g.fcart[1] && g.fcart[0] == g.fcart[2];
+#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                           \
+  return iso ? launch_plane_t<KK, TXX, TYY, true>(g, t, src, dst, s, launches)  \
+             : launch_plane_t<KK, TXX, TYY, false>(g, t, src, dst, s, launches)
+  static int shape = -1;  // MF_TILE=16x2 selects the wide tile (experiments)
+  if (shape < 0) {
+    const char *e = getenv("MF_TILE");
+    shape = (e && !strcmp(e, "16x2")) ? 1 : 0;
+  }
+  switch (g.k) {
+    case 2: MF_PLANE_LAUNCH(2, 8, 8);
+    case 3: MF_PLANE_LAUNCH(3, 8, 4);
+    case 4:
+      if (shape == 1) MF_PLANE_LAUNCH(4, 16, 2);
+      MF_PLANE_LAUNCH(4, 8, 4);
+  }
+#undef MF_PLANE_LAUNCH
+  return cudaErrorNotSupported;
+}
+
+}  // namespace mf

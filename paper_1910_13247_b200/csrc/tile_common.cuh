@@ -1,0 +1,238 @@
+// tile_common.cuh -- pieces shared by the Cartesian tile kernels (kernels_tile.cu,
+// kernels_plane.cu): even-odd 1D products, the kernel parameter block, the init
+// kernel for shared planes / Dirichlet rows, cp.async helper and host set-up.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.h"
+
+namespace mf {
+
+constexpr int kMaxH = 5;  // (kMaxN + 1) / 2
+
+struct EOMat {
+  double E[kMaxH][kMaxH];  // even part (rows i < h, cols j < h; col m = middle for odd n)
+  double O[kMaxH][kMaxH];  // odd part (rows/cols < n/2)
+};
+
+// sm_100 DFMA takes no constant-bank operand: coefficients live in the 64-entry
+// uniform register file, so only two EO matrices are kept -- M and K = f_x K_ref --
+// and Ky' = ry K, Kz' = rz K are applied by scaling the data (ry = rz = 1 on
+// cubes, where the ISO template skips the scaling).
+struct TileParams {
+  EOMat M, K;
+  double ry, rz;
+  int64_t Nx, Ny, Nz;  // local node counts
+  int ncx, ncy, ncz;   // local cell counts
+  int ntx, nty, nch, LZ;
+  uint32_t dirichlet;
+  int skip_top_identity;
+  unsigned long long *prof;  // debug counters [2][8] or null
+};
+
+// ---- even-odd 1D products --------------------------------------------------
+template <int N>
+struct EO {
+  static constexpr int m = N / 2, h = (N + 1) / 2;
+};
+
+template <int N>
+__device__ __forceinline__ void eo_split(const double *u, double *e, double *o) {
+  constexpr int m = N / 2;
+#pragma unroll
+  for (int j = 0; j < m; ++j) {
+    e[j] = u[j] + u[N - 1 - j];
+    o[j] = u[j] - u[N - 1 - j];
+  }
+  if (N & 1) e[m] = u[m];
+}
+
+// ve += E e, vo += O o
+template <int N>
+__device__ __forceinline__ void eo_acc(const EOMat &A, const double *e, const double *o, double *ve, double *vo) {
+  constexpr int m = N / 2, h = (N + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < h; ++i)
+#pragma unroll
+    for (int j = 0; j < h; ++j) ve[i] = fma(A.E[i][j], e[j], ve[i]);
+#pragma unroll
+  for (int i = 0; i < m; ++i)
+#pragma unroll
+    for (int j = 0; j < m; ++j) vo[i] = fma(A.O[i][j], o[j], vo[i]);
+}
+
+template <int N>
+__device__ __forceinline__ void eo_first(const EOMat &A, const double *e, const double *o, double *ve, double *vo) {
+  constexpr int m = N / 2, h = (N + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < h; ++i) {
+    ve[i] = A.E[i][0] * e[0];
+#pragma unroll
+    for (int j = 1; j < h; ++j) ve[i] = fma(A.E[i][j], e[j], ve[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < m; ++i) {
+    vo[i] = A.O[i][0] * o[0];
+#pragma unroll
+    for (int j = 1; j < m; ++j) vo[i] = fma(A.O[i][j], o[j], vo[i]);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void eo_combine(const double *ve, const double *vo, double *v) {
+  constexpr int m = N / 2;
+#pragma unroll
+  for (int i = 0; i < m; ++i) {
+    v[i] = ve[i] + vo[i];
+    v[N - 1 - i] = ve[i] - vo[i];
+  }
+  if (N & 1) v[m] = ve[m];
+}
+
+
+// ---- init: shared-edge / chunk-plane nodes and Dirichlet rows ---------------
+// dst = src on constrained nodes (except the top plane of a non-last slab),
+// 0 on every other node that several blocks add into.  The planes are given as
+// arithmetic families (axis, first coordinate, stride, count).
+struct PlaneSet {
+  int axis[12], count[12];
+  int64_t c0[12], stride[12];
+  int nfam;
+};
+
+static __global__ void k_tile_init(const __grid_constant__ TileParams P, const __grid_constant__ PlaneSet ps,
+                            const double *__restrict__ src, double *__restrict__ dst) {
+  int pl = blockIdx.y, f = 0;
+  while (f < ps.nfam && pl >= ps.count[f]) pl -= ps.count[f++];
+  if (f >= ps.nfam) return;
+  const int axis = ps.axis[f];
+  const int c = (int)(ps.c0[f] + ps.stride[f] * pl);
+  const int Nx = (int)P.Nx, Ny = (int)P.Ny, Nz = (int)P.Nz;
+  // the plane is a set of lines (one per block iteration), nodes of a line per thread:
+  // x-plane: lines gz, nodes gy (stride Nx); y-plane: lines gz, nodes gx; z-plane: lines gy, nodes gx
+  const int nlines = axis == 2 ? Ny : Nz, nnodes = axis == 0 ? Ny : Nx;
+  const uint32_t d = P.dirichlet;
+  for (int line = blockIdx.x; line < nlines; line += gridDim.x) {
+    for (int a = threadIdx.x; a < nnodes; a += blockDim.x) {
+      int gx, gy, gz;
+      if (axis == 0) { gx = c; gy = a; gz = line; }
+      else if (axis == 1) { gx = a; gy = c; gz = line; }
+      else { gx = a; gy = line; gz = c; }
+      const bool cons = ((d & 1u) && gx == 0) || ((d & 2u) && gx == Nx - 1) || ((d & 4u) && gy == 0) ||
+                        ((d & 8u) && gy == Ny - 1) || ((d & 16u) && gz == 0) || ((d & 32u) && gz == Nz - 1);
+      const int64_t gi = ((int64_t)gz * Ny + gy) * Nx + gx;
+      const bool ident = cons && !(P.skip_top_identity && gz == Nz - 1);
+      dst[gi] = ident ? __ldg(src + gi) : 0.0;
+    }
+  }
+}
+
+// 8-byte cp.async global -> shared; src_bytes = 0 writes zeros without reading
+__device__ __forceinline__ void cp_async8z(double *smem, const double *gmem, unsigned src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
+}
+
+// ---- host side -------------------------------------------------------------------
+static inline void to_eo(int n, const double A[kMaxN][kMaxN], EOMat *out) {
+  std::memset(out, 0, sizeof(EOMat));
+  const int m = n / 2, h = (n + 1) / 2;
+  for (int i = 0; i < h; ++i) {
+    for (int j = 0; j < m; ++j) out->E[i][j] = 0.5 * (A[i][j] + A[i][n - 1 - j]);
+    if (n & 1) out->E[i][m] = A[i][m];
+  }
+  // the middle row of an odd n: v[m] = sum_{j<m} A[m][j] e[j] + A[m][m] u[m] (e unhalved)
+  if (n & 1)
+    for (int j = 0; j < m; ++j) out->E[m][j] = A[m][j];
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) out->O[i][j] = 0.5 * (A[i][j] - A[i][n - 1 - j]);
+}
+
+// 1D reference mass M = S^T W S and stiffness K_ref = D^T W D from the tables
+// (Gauss(k+1) integrates both exactly), then P.M = EO(M), P.K = EO(f_x K_ref),
+// ry = f_y / f_x, rz = f_z / f_x, and the mesh sizes.
+static inline void tile_params_common(const Geo &g, const Tables &t, int TX, int TY, TileParams *P) {
+  const int N = g.k + 1;
+  std::memset(P, 0, sizeof(*P));
+  double M[kMaxN][kMaxN] = {}, Kx[kMaxN][kMaxN] = {};
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      long double mm = 0, kk = 0;
+      for (int q = 0; q < N; ++q) {
+        mm += (long double)t.w[q] * t.S[q][i] * t.S[q][j];
+        kk += (long double)t.w[q] * t.D[q][i] * t.D[q][j];
+      }
+      M[i][j] = (double)mm;
+      Kx[i][j] = (double)(g.fcart[0] * kk);
+    }
+  to_eo(N, M, &P->M);
+  to_eo(N, Kx, &P->K);
+  P->ry = g.fcart[1] / g.fcart[0];
+  P->rz = g.fcart[2] / g.fcart[0];
+  P->Nx = g.N[0];
+  P->Ny = g.N[1];
+  P->Nz = g.N[2];
+  P->ncx = (int)g.nc[0];
+  P->ncy = (int)g.nc[1];
+  P->ncz = (int)g.nc[2];
+  P->ntx = (P->ncx + TX - 1) / TX;
+  P->nty = (P->ncy + TY - 1) / TY;
+  P->dirichlet = g.dirichlet;
+  P->skip_top_identity = g.skip_top_identity;
+}
+
+// z-chunk length balancing the (tile, chunk) items against the resident-block slots
+static inline void tile_choose_chunks(TileParams *P, int slots, double per_chunk_overhead) {
+  const int tiles = P->ntx * P->nty;
+  int best_nch = 1;
+  double best = 1e30;
+  for (int nch = 1; nch <= P->ncz; ++nch) {
+    const int LZ = (P->ncz + nch - 1) / nch;
+    const int real_nch = (P->ncz + LZ - 1) / LZ;
+    const double waves = std::ceil((double)tiles * real_nch / slots);
+    const double cost = waves * (LZ + per_chunk_overhead);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_nch = real_nch;
+    }
+  }
+  P->LZ = (P->ncz + best_nch - 1) / best_nch;
+  P->nch = (P->ncz + P->LZ - 1) / P->LZ;
+}
+
+// init kernel: planes shared between blocks (internal tile edges, chunk planes)
+// get 0, Dirichlet faces get the identity value
+static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, int K, int TX, int TY,
+                                           const double *src, double *dst, cudaStream_t s, int64_t *launches) {
+  PlaneSet ps;
+  std::memset(&ps, 0, sizeof(ps));
+  int total = 0;
+  auto fam = [&](int axis, int64_t c0, int64_t stride, int count) {
+    if (count <= 0) return;
+    ps.axis[ps.nfam] = axis;
+    ps.c0[ps.nfam] = c0;
+    ps.stride[ps.nfam] = stride;
+    ps.count[ps.nfam++] = count;
+    total += count;
+  };
+  fam(0, (int64_t)K * TX, (int64_t)K * TX, P.ntx - 1);
+  fam(1, (int64_t)K * TY, (int64_t)K * TY, P.nty - 1);
+  fam(2, (int64_t)K * P.LZ, (int64_t)K * P.LZ, P.nch - 1);
+  if (g.dirichlet & 1u) fam(0, 0, 1, 1);
+  if (g.dirichlet & 2u) fam(0, P.Nx - 1, 1, 1);
+  if (g.dirichlet & 4u) fam(1, 0, 1, 1);
+  if (g.dirichlet & 8u) fam(1, P.Ny - 1, 1, 1);
+  if (g.dirichlet & 16u) fam(2, 0, 1, 1);
+  if ((g.dirichlet & 32u) || g.skip_top_identity) fam(2, P.Nz - 1, 1, 1);
+  if (total == 0) return cudaSuccess;
+  ++*launches;
+  dim3 grid((unsigned)std::min<int64_t>(std::max(P.Ny, P.Nz), 256), total);
+  k_tile_init<<<grid, 128, 0, s>>>(P, ps, src, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace mf

@@ -82,14 +82,14 @@ TILE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("variant", ["general", "tile"])
+@pytest.mark.parametrize("variant", ["general", "tile", "plane"])
 @pytest.mark.parametrize("case", TILE_CASES, ids=_id)
 def test_cartesian_variants_match_oracle(case, variant, torch):
     p = oracle_problem(case)
     A = oracle.CSR(p)
     op = cuda_operator(case)
     op.set_variant(variant)
-    assert op.info()["apply_variant"] == {"general": 1, "tile": 2}[variant]
+    assert op.info()["apply_variant"] == {"general": 1, "tile": 2, "plane": 3}[variant]
     for s in (1, 2, 3):
         x = seeded(A.n, s)
         y_ref = A @ x

@@ -66,7 +66,9 @@ __global__ void k_copy(const double *__restrict__ a, double *__restrict__ b, lon
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
-int main() {
+int lat_main();
+int main(int argc, char **argv) {
+  if (argc > 1) return lat_main();
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
   printf("{\"device\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"smem_per_sm\": %zu, \"mem_bytes\": %zu, \"clock_khz\": %d}\n",
@@ -150,5 +152,39 @@ int main() {
     }
     printf("{\"copy_gbps\": %.1f}\n", 16.0 * n / best / 1e6);
   }
+  return 0;
+}
+
+// ---- DFMA latency / ILP sweep: one warp per SM, `chains` independent dependent chains
+template <int CH>
+__global__ void k_dfma_lat(double *out, int iters, long long *cyc) {
+  double x[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) x[j] = threadIdx.x * 1e-3 + j;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) x[j] = fma(x[j], 1.0000001, 1e-9);
+  }
+  long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) s += x[j];
+  if (s == 12345.678) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
+int lat_main() {
+  double *buf;
+  long long *cyc, h;
+  cudaMalloc(&buf, 1024);
+  cudaMalloc(&cyc, 8);
+  const int iters = 4096;
+#define LAT(CH, W)                                                                                   \
+  k_dfma_lat<CH><<<148, 32 * W>>>(buf, iters, cyc);                                                 \
+  cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);                                                    \
+  printf("{\"dfma_chains\": %d, \"warps_per_sm\": %d, \"cycles_per_dfma_per_warp\": %.2f}\n", CH, W, \
+         (double)h / iters / CH);
+  LAT(1, 1) LAT(2, 1) LAT(4, 1) LAT(8, 1) LAT(1, 4) LAT(2, 4) LAT(4, 4) LAT(8, 4) LAT(2, 8) LAT(4, 8)
   return 0;
 }
