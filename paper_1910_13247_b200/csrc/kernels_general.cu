@@ -29,13 +29,29 @@ struct Shape {
   static constexpr int NV = NP * N;                // values per cell
 };
 
-// offset of entry i of pencil p along direction dir inside an N^DIM cell tensor (x fastest)
+// Shared-memory slot of local node (x, y, z) of a cell tensor.  Lexicographic, except
+// for 3D with N = 4 (Q3): s = 16 z + 4 ((y + z) & 3) + ((x + z) & 3) puts the 16
+// pencils of a half-warp on 16 distinct banks in every sweep direction and the 16
+// nodes of a z-plane likewise (a Latin-cube map), with no padding.
+template <int DIM, int N>
+__device__ __forceinline__ int sidx(int x, int y, int z) {
+  if (DIM == 3 && N == 4) return 16 * z + 4 * ((y + z) & 3) + ((x + z) & 3);
+  return DIM == 3 ? (z * N + y) * N + x : y * N + x;
+}
+
+// slot of entry i of pencil p along direction dir (pencils enumerate the other two axes, x fastest)
 template <int DIM, int N>
 __device__ __forceinline__ int pen_off(int dir, int p, int i) {
-  if (DIM == 2) return dir == 0 ? p * N + i : i * N + p;
-  if (dir == 0) return p * N + i;                          // p = z*N + y
-  if (dir == 1) return (p / N) * N * N + i * N + (p % N);  // p = z*N + x
-  return i * N * N + p;                                    // p = y*N + x
+  if (DIM == 2) return dir == 0 ? sidx<DIM, N>(i, p, 0) : sidx<DIM, N>(p, i, 0);
+  if (dir == 0) return sidx<DIM, N>(i, p % N, p / N);  // p = z*N + y
+  if (dir == 1) return sidx<DIM, N>(p % N, i, p / N);  // p = z*N + x
+  return sidx<DIM, N>(p % N, p / N, i);                // p = y*N + x
+}
+
+// slot of the lexicographic local node / quadrature point i
+template <int DIM, int N>
+__device__ __forceinline__ int nidx(int i) {
+  return sidx<DIM, N>(i % N, (i / N) % N, DIM == 3 ? i / (N * N) : 0);
 }
 
 // out[i] = sum_j M[i][j] in[j]   (TR: sum_j M[j][i] in[j])
@@ -106,6 +122,56 @@ __device__ __forceinline__ double coeff_var(const double x[3], int dim) {
   return 1.0 / (0.05 + 2.0 * r2);  // R5
 }
 
+// per-cell data of an apply block, computed once per cell
+struct CellInfo {
+  long long base;  // local DoF index of the cell's node (0,0,0)
+  int cx, cy, cz;
+  int flags;  // bits 0-5: the cell touches constrained face x-,x+,y-,y+,z-,z+;
+              // 6-8: cx / cy / cz == 0 (identity-row owner rule); 9: skip identity on its top plane; 10: valid
+};
+
+template <int DIM, int K>
+__device__ __forceinline__ CellInfo cell_info(const Geo &g, int64_t cell, int64_t ncells) {
+  CellInfo ci;
+  ci.flags = 0;
+  ci.base = 0;
+  ci.cx = ci.cy = ci.cz = 0;
+  if (cell >= ncells) return ci;
+  const int64_t cx = cell % g.nc[0], r = cell / g.nc[0];
+  const int64_t cy = r % g.nc[1], cz = r / g.nc[1];
+  ci.cx = (int)cx;
+  ci.cy = (int)cy;
+  ci.cz = (int)cz;
+  ci.base = ((int64_t)K * cz * g.N[1] + (int64_t)K * cy) * g.N[0] + (int64_t)K * cx;
+  const uint32_t d = g.dirichlet;
+  int f = 1 << 10;
+  if ((d & 1u) && cx == 0) f |= 1;
+  if ((d & 2u) && cx == g.nc[0] - 1) f |= 2;
+  if ((d & 4u) && cy == 0) f |= 4;
+  if ((d & 8u) && cy == g.nc[1] - 1) f |= 8;
+  if (DIM == 3 && (d & 16u) && cz == 0) f |= 16;
+  if (DIM == 3 && (d & 32u) && cz == g.nc[2] - 1) f |= 32;
+  if (cx == 0) f |= 64;
+  if (cy == 0) f |= 128;
+  if (DIM == 2 || cz == 0) f |= 256;
+  if (DIM == 3 && g.skip_top_identity && cz == g.nc[2] - 1) f |= 512;
+  ci.flags = f;
+  return ci;
+}
+
+// node i of a cell: local DoF index, constrained flag, identity-row owner flag
+template <int DIM, int N>
+__device__ __forceinline__ void node_of(const CellInfo &ci, int i, int64_t Nx, int64_t plane, int64_t &gi,
+                                        bool &cons, bool &owner) {
+  const int lx = i % N, ly = (i / N) % N, lz = DIM == 3 ? i / (N * N) : 0;
+  gi = ci.base + (DIM == 3 ? lz * plane : 0) + ly * Nx + lx;
+  const int f = ci.flags;
+  cons = ((f & 1) && lx == 0) || ((f & 2) && lx == N - 1) || ((f & 4) && ly == 0) || ((f & 8) && ly == N - 1) ||
+         ((f & 16) && lz == 0) || ((f & 32) && lz == N - 1);
+  owner = (lx >= 1 || (f & 64)) && (ly >= 1 || (f & 128)) && (DIM == 2 || lz >= 1 || (f & 256)) &&
+          !((f & 512) && lz == N - 1);
+}
+
 // ---------------------------------------------------------------------------
 // GEOM: 0 = affine box, constant coefficient; 1 = affine box, variable
 // coefficient evaluated at x_q on the fly; 2 = stored metric G (curved).
@@ -117,21 +183,47 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
   constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
   constexpr int CS = (DIM + 1) * NV;  // doubles of shared memory per cell
   extern __shared__ double sm[];
+  CellInfo *info = reinterpret_cast<CellInfo *>(sm + cpb * CS);
   const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
   const int64_t cell0 = (int64_t)blockIdx.x * cpb;
+  const int64_t Nx = g.N[0], plane = g.N[0] * g.N[1];
+
+  // per-cell data, one 64-bit division per cell instead of one per node
+  for (int cl = threadIdx.x; cl < cpb; cl += blockDim.x) info[cl] = cell_info<DIM, K>(g, cell0 + cl, ncells);
+  __syncthreads();
 
   // a3: gather
   for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
     const int cl = idx / NV, i = idx - cl * NV;
-    const int64_t cell = cell0 + cl;
+    const CellInfo ci = info[cl];
     double v = 0.0;
-    if (cell < ncells) {
-      CellIdx ci = cell_coords(g, cell);
-      int64_t m[3];
-      int64_t gi = node_index<DIM, N>(g, ci, i, m);
-      if (!is_constrained(g, m)) v = __ldg(src + gi);
+    if (ci.flags) {
+      int64_t gi;
+      bool cons, owner;
+      node_of<DIM, N>(ci, i, Nx, plane, gi, cons, owner);
+      if (!cons) v = __ldg(src + gi);
     }
-    sm[cl * CS + i] = v;
+    sm[cl * CS + nidx<DIM, N>(i)] = v;
+  }
+  // a2 data of a5: optionally the stored metric of this thread's quadrature points
+  // is loaded into registers here so its HBM latency overlaps the forward sweeps
+  // (A thread owns at most N quadrature points, blockDim >= cpb * NP).  Measured on
+  // cfg 4 the extra registers cost more occupancy than the overlap gains: off.
+  constexpr bool PREF = false;
+  constexpr int NGC = DIM == 3 ? 6 : 3;
+  double gm[GEOM == 2 && PREF ? N : 1][NGC];
+  if (GEOM == 2 && PREF) {
+    const int64_t stride = ncells * NV;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      const int idx = threadIdx.x + r * blockDim.x;
+      const int c2 = idx / NV, q = idx - c2 * NV;
+      const int64_t cell = cell0 + c2;
+      const bool ok = idx < cpb * NV && cell < ncells;
+      const double *Gm = metric + (ok ? cell * NV + q : 0);
+#pragma unroll
+      for (int c = 0; c < NGC; ++c) gm[r][c] = ok ? __ldg(Gm + c * stride) : 0.0;
+    }
   }
   __syncthreads();
 
@@ -161,40 +253,46 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
   __syncthreads();
 
   // a5: quadrature-point operation
-  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    const int idx = threadIdx.x + r * blockDim.x;
+    if (idx >= cpb * NV) break;
     const int c2 = idx / NV, q = idx - c2 * NV;
-    const int64_t cell = cell0 + c2;
     double *Uc = sm + c2 * CS;
     const int q0 = q % N, q1 = (q / N) % N, q2 = DIM == 3 ? q / (N * N) : 0;
     double gr[3], tt[3];
+    const int qs = nidx<DIM, N>(q);
 #pragma unroll
-    for (int e = 0; e < DIM; ++e) gr[e] = Uc[(e + 1) * NV + q];
+    for (int e = 0; e < DIM; ++e) gr[e] = Uc[(e + 1) * NV + qs];
     if (GEOM == 2) {
-      if (cell < ncells) {
-        const int64_t stride = ncells * NV;
-        const double *Gm = metric + cell * NV + q;
-        if (DIM == 3) {
-          double G00 = __ldg(Gm), G01 = __ldg(Gm + stride), G02 = __ldg(Gm + 2 * stride),
-                 G11 = __ldg(Gm + 3 * stride), G12 = __ldg(Gm + 4 * stride), G22 = __ldg(Gm + 5 * stride);
-          tt[0] = G00 * gr[0] + G01 * gr[1] + G02 * gr[2];
-          tt[1] = G01 * gr[0] + G11 * gr[1] + G12 * gr[2];
-          tt[2] = G02 * gr[0] + G12 * gr[1] + G22 * gr[2];
-        } else {
-          double G00 = __ldg(Gm), G01 = __ldg(Gm + stride), G11 = __ldg(Gm + 2 * stride);
-          tt[0] = G00 * gr[0] + G01 * gr[1];
-          tt[1] = G01 * gr[0] + G11 * gr[1];
-        }
+      double G[NGC];
+      if (PREF) {
+#pragma unroll
+        for (int c = 0; c < NGC; ++c) G[c] = gm[PREF ? r : 0][c];
       } else {
-        tt[0] = tt[1] = tt[2] = 0.0;
+        const int64_t cell = cell0 + c2;
+        const bool ok = cell < ncells;
+        const double *Gm = metric + (ok ? cell * NV + q : 0);
+#pragma unroll
+        for (int c = 0; c < NGC; ++c) G[c] = ok ? __ldg(Gm + c * (ncells * NV)) : 0.0;
+      }
+      if (DIM == 3) {
+        tt[0] = G[0] * gr[0] + G[1] * gr[1] + G[2] * gr[2];
+        tt[1] = G[1] * gr[0] + G[3] * gr[1] + G[4] * gr[2];
+        tt[2] = G[2] * gr[0] + G[4] * gr[1] + G[5] * gr[2];
+      } else {
+        tt[0] = G[0] * gr[0] + G[1] * gr[1];
+        tt[1] = G[1] * gr[0] + G[2] * gr[1];
       }
     } else {
       double W = t.w[q0] * t.w[q1] * (DIM == 3 ? t.w[q2] : 1.0);
       if (GEOM == 1) {
-        CellIdx ci = cell_coords(g, cell < ncells ? cell : 0);
+        const CellInfo ci = info[c2];
         double x[3];
         const int qq[3] = {q0, q1, q2};
+        const int cc[3] = {ci.cx, ci.cy, ci.cz};
         for (int d = 0; d < DIM; ++d) {
-          double cg = (double)(d == 2 ? ci.c[2] + g.cz0 : ci.c[d]);
+          double cg = (double)(d == 2 ? cc[2] + g.cz0 : cc[d]);
           x[d] = g.lo[d] + g.h[d] * (cg + t.xi[qq[d]]);
         }
         double vol = g.h[0] * g.h[1] * (DIM == 3 ? g.h[2] : 1.0);
@@ -207,7 +305,7 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
       }
     }
 #pragma unroll
-    for (int e = 0; e < DIM; ++e) Uc[(e + 1) * NV + q] = tt[e];
+    for (int e = 0; e < DIM; ++e) Uc[(e + 1) * NV + qs] = tt[e];
   }
   __syncthreads();
 
@@ -242,15 +340,15 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
   // a7: scatter-add and identity rows
   for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
     const int c2 = idx / NV, i = idx - c2 * NV;
-    const int64_t cell = cell0 + c2;
-    if (cell >= ncells) continue;
-    CellIdx ci = cell_coords(g, cell);
-    int64_t m[3];
-    int64_t gi = node_index<DIM, N>(g, ci, i, m);
-    if (is_constrained(g, m)) {
-      if (owner_of<DIM, N>(g, ci, i, m)) dst[gi] = __ldg(src + gi);
+    const CellInfo ci = info[c2];
+    if (!ci.flags) continue;
+    int64_t gi;
+    bool cons, owner;
+    node_of<DIM, N>(ci, i, Nx, plane, gi, cons, owner);
+    if (cons) {
+      if (owner) dst[gi] = __ldg(src + gi);
     } else {
-      atomicAdd(dst + gi, sm[c2 * CS + i]);
+      atomicAdd(dst + gi, sm[c2 * CS + nidx<DIM, N>(i)]);
     }
   }
 }
@@ -259,7 +357,7 @@ template <int DIM, int K>
 static int cells_per_block() {
   constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
   int cpb = 256 / NP;
-  const int cs = (DIM + 1) * NV * 8;
+  const int cs = (DIM + 1) * NV * 8 + (int)sizeof(CellInfo);
   while (cpb > 1 && cpb * cs > 48 * 1024) --cpb;
   return cpb < 1 ? 1 : cpb;
 }
@@ -272,7 +370,7 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
   int threads = ((cpb * NP + 31) / 32) * 32;
   const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
   const int64_t blocks = (ncells + cpb - 1) / cpb;
-  const size_t smem = (size_t)cpb * (DIM + 1) * NV * sizeof(double);
+  const size_t smem = (size_t)cpb * ((DIM + 1) * NV * sizeof(double) + sizeof(CellInfo));
   if (blocks == 0) return cudaSuccess;
   k_apply_general<DIM, K, GEOM><<<(unsigned)blocks, threads, smem, s>>>(t, g, src, dst, metric, cpb);
   return cudaGetLastError();
@@ -485,7 +583,7 @@ __global__ void __launch_bounds__(256) k_diagonal(const __grid_constant__ Tables
           }
         }
       }
-      sm[c2 * 2 * NV + NV + q] = v;
+      sm[c2 * 2 * NV + NV + nidx<DIM, N>(q)] = v;
     }
     __syncthreads();
     for (int e = 0; e < DIM; ++e) {
@@ -522,7 +620,7 @@ __global__ void __launch_bounds__(256) k_diagonal(const __grid_constant__ Tables
     if (is_constrained(g, m)) {
       if (owner_of<DIM, N>(g, ci, i, m)) diag[gi] = 1.0;
     } else {
-      atomicAdd(diag + gi, sm[c2 * 2 * NV + i]);
+      atomicAdd(diag + gi, sm[c2 * 2 * NV + nidx<DIM, N>(i)]);
     }
   }
 }
