@@ -100,28 +100,51 @@ __device__ __forceinline__ void eo_combine(const double *ve, const double *vo, d
 // arithmetic families (axis, first coordinate, stride, count).
 struct PlaneSet {
   int axis[12], count[12];
-  int64_t c0[12], stride[12];
+  int64_t c0[12], stride[12], lines[12];  // lines = count x lines per plane
+  int64_t total_lines;
   int nfam;
 };
 
-static __global__ void k_tile_init(const __grid_constant__ TileParams P, const __grid_constant__ PlaneSet ps,
-                            const double *__restrict__ src, double *__restrict__ dst) {
-  int pl = blockIdx.y, f = 0;
-  while (f < ps.nfam && pl >= ps.count[f]) pl -= ps.count[f++];
-  if (f >= ps.nfam) return;
-  const int axis = ps.axis[f];
-  const int c = (int)(ps.c0[f] + ps.stride[f] * pl);
+static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant__ TileParams P,
+                                                           const __grid_constant__ PlaneSet ps,
+                                                           const double *__restrict__ src, double *__restrict__ dst) {
+  // one warp per line of a plane (x-plane: line gz, nodes gy; y-plane: line gz,
+  // nodes gx; z-plane: line gy, nodes gx), warps grid-stride over all lines
   const int Nx = (int)P.Nx, Ny = (int)P.Ny, Nz = (int)P.Nz;
-  // the plane is a set of lines (one per block iteration), nodes of a line per thread:
-  // x-plane: lines gz, nodes gy (stride Nx); y-plane: lines gz, nodes gx; z-plane: lines gy, nodes gx
-  const int nlines = axis == 2 ? Ny : Nz, nnodes = axis == 0 ? Ny : Nx;
   const uint32_t d = P.dirichlet;
-  for (int line = blockIdx.x; line < nlines; line += gridDim.x) {
-    for (int a = threadIdx.x; a < nnodes; a += blockDim.x) {
-      int gx, gy, gz;
-      if (axis == 0) { gx = c; gy = a; gz = line; }
-      else if (axis == 1) { gx = a; gy = c; gz = line; }
-      else { gx = a; gy = line; gz = c; }
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t L = warp; L < ps.total_lines; L += nwarps) {
+    int f = 0;
+    int64_t l = L;
+    while (f < ps.nfam - 1 && l >= ps.lines[f]) l -= ps.lines[f++];
+    const int axis = ps.axis[f];
+    const int nlines = axis == 2 ? Ny : Nz, nnodes = axis == 0 ? Ny : Nx;
+    const int pl = (int)(l / nlines), line = (int)(l - (int64_t)pl * nlines);
+    const int c = (int)(ps.c0[f] + ps.stride[f] * pl);
+    if (axis == 0 && c >= 4 && c + 4 < Nx && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
+      // strided x-plane nodes: write the whole aligned 32-byte sector around each
+      // node instead of 8 bytes of it (no partial-sector writes).  The sector
+      // stays inside the row, off the x faces (4 <= c < Nx - 4); its other nodes are owned by one
+      // block, which overwrites them later, so they get the value every writer
+      // agrees on (the identity on constrained nodes, else 0).
+      for (int a = lane; a < nnodes; a += 32) {
+        const int64_t row = ((int64_t)line * Ny + a) * Nx;
+        const int64_t g0 = (row + c) & ~(int64_t)3;
+        const bool ycons = ((d & 4u) && a == 0) || ((d & 8u) && a == Ny - 1) || ((d & 16u) && line == 0) ||
+                           ((d & 32u) && line == Nz - 1);
+        const bool ident = ycons && !(P.skip_top_identity && line == Nz - 1);
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = ident ? __ldg(src + g0 + q) : 0.0;
+        double2 *p = reinterpret_cast<double2 *>(dst + g0);
+        p[0] = make_double2(v[0], v[1]);
+        p[1] = make_double2(v[2], v[3]);
+      }
+      continue;
+    }
+    for (int a = lane; a < nnodes; a += 32) {
+      const int gx = axis == 0 ? c : a, gy = axis == 0 ? a : (axis == 1 ? c : line), gz = axis == 2 ? c : line;
       const bool cons = ((d & 1u) && gx == 0) || ((d & 2u) && gx == Nx - 1) || ((d & 4u) && gy == 0) ||
                         ((d & 8u) && gy == Ny - 1) || ((d & 16u) && gz == 0) || ((d & 32u) && gz == Nz - 1);
       const int64_t gi = ((int64_t)gz * Ny + gy) * Nx + gx;
@@ -216,7 +239,8 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
     ps.axis[ps.nfam] = axis;
     ps.c0[ps.nfam] = c0;
     ps.stride[ps.nfam] = stride;
-    ps.count[ps.nfam++] = count;
+    ps.count[ps.nfam] = count;
+    ps.lines[ps.nfam++] = (int64_t)count * (axis == 2 ? P.Ny : P.Nz);
     total += count;
   };
   fam(0, (int64_t)K * TX, (int64_t)K * TX, P.ntx - 1);
@@ -230,8 +254,9 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
   if ((g.dirichlet & 32u) || g.skip_top_identity) fam(2, P.Nz - 1, 1, 1);
   if (total == 0) return cudaSuccess;
   ++*launches;
-  dim3 grid((unsigned)std::min<int64_t>(std::max(P.Ny, P.Nz), 256), total);
-  k_tile_init<<<grid, 128, 0, s>>>(P, ps, src, dst);
+  for (int f = 0; f < ps.nfam; ++f) ps.total_lines += ps.lines[f];
+  const int blocks = (int)std::min<int64_t>((ps.total_lines + 7) / 8, 148 * 8);
+  k_tile_init<<<blocks, 256, 0, s>>>(P, ps, src, dst);
   return cudaGetLastError();
 }
 
