@@ -107,9 +107,11 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   };
 
   // cp.async of node planes l0..K of layer cz of item I (this thread's columns) into the stage
+  // (constrained nodes are zero-filled: their addresses are valid vector entries,
+  // only the byte count drops to 0)
   auto prefetch = [&](const Item &I, int cz, int l0) {
     const double *sp0 = src + I.base0 + (int64_t)K * (cz - I.cz_begin) * plane;
-    const int64_t gzb = (int64_t)K * cz;
+    const bool zlo = z_lo_c && cz == 0, zhi = z_hi_c && cz == P.ncz - 1;  // planes l = 0 / l = K
     const bool own_ok = ccx < I.nvx && ccy < I.nvy;
     const int y = K * ccy + jr;
     const bool ycons = (d & 4u) && K * I.cy0 + y == 0;
@@ -117,23 +119,23 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
     int ex = 0, ey = 0;
     const bool has_e = edge_xy(I, ex, ey);
     const bool e_ok = has_e && !xy_cons(I, ex, ey);
+    const double *go = sp0 + y * Nx + K * ccx, *ge = sp0 + ey * Nx + ex;
+    double *so = Us + y * NXc + K * ccx, *se = Us + ey * NXc + ex;
 #pragma unroll
     for (int l = 0; l <= K; ++l) {
-      if (l < l0) continue;
-      const bool zc = (z_lo_c && gzb + l == 0) || (z_hi_c && gzb + l == P.Nz - 1);
-      const double *spl = sp0 + l * plane;
-      double *ul = Us + l * SPL;
-      if (own_ok) {
+      if (l >= l0) {
+        const bool zc = (l == 0 && zlo) || (l == K && zhi);
+        if (own_ok) {
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          const bool ok = !zc && !ycons && !(i == 0 && xcons0);
-          cp_async8z(ul + y * NXc + K * ccx + i, ok ? spl + y * Nx + K * ccx + i : src, ok ? 8u : 0u);
+          for (int i = 0; i < K; ++i) {
+            const bool ok = !zc && !ycons && !(i == 0 && xcons0);
+            cp_async8z(so + l * SPL + i, go + i, ok ? 8u : 0u);
+          }
         }
+        if (has_e) cp_async8z(se + l * SPL, ge, (e_ok && !zc) ? 8u : 0u);
       }
-      if (has_e) {
-        const bool ok = e_ok && !zc;
-        cp_async8z(ul + ey * NXc + ex, ok ? spl + ey * Nx + ex : src, ok ? 8u : 0u);
-      }
+      go += plane;
+      ge += plane;
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -183,8 +185,10 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   };
 
   // ---- z-sweep of one column: v = Mz P + Kz' Q (even-odd), carries, stores
+  // zm / am: the layer's planes l that are z-constrained / shared with the
+  // neighbouring z-chunk (bit l, warp-uniform)
   auto zcolumn = [&](const double *pb, const double *qb, double &vcar, bool first, bool last, bool cons, bool shared,
-                     double *out, int64_t gzb, int chunk) {
+                     double *out, uint32_t zm, uint32_t am) {
     double e[h], o[h], ve[h], vo[h], v[N];
     eo_split<N>(pb, e, o);
     eo_first<N>(P.M, e, o, ve, vo);
@@ -204,12 +208,11 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
 #pragma unroll
     for (int l = 0; l <= K; ++l) {
       if (l == K && !last) break;  // carried to the next layer
-      const int64_t gz = gzb + l;
-      if ((z_lo_c && gz == 0) || (z_hi_c && gz == P.Nz - 1)) continue;
-      const bool at = shared || (l == 0 && first && chunk > 0) || (l == K && chunk < P.nch - 1);
-      double *p = out + l * plane;
-      if (at) atomicAdd(p, v[l]);
-      else *p = v[l];
+      if (!((zm >> l) & 1u)) {
+        if (shared || ((am >> l) & 1u)) atomicAdd(out, v[l]);
+        else *out = v[l];
+      }
+      out += plane;
     }
   };
 
@@ -278,7 +281,8 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
       } else if (next < nitems) {
         prefetch(item_of(next), item_of(next).cz_begin, 0);
       }
-      const int64_t gzb = (int64_t)K * cz;
+      const uint32_t zm = ((z_lo_c && cz == 0) ? 1u : 0u) | ((z_hi_c && cz == P.ncz - 1) ? 1u << K : 0u);
+      const uint32_t am = ((first && chunk > 0) ? 1u : 0u) | ((last && chunk < P.nch - 1) ? 1u << K : 0u);
       double *outl = dst + base0 + (int64_t)K * (cz - cz_begin) * plane;
       if (own_ok) {
 #pragma unroll
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
           pcar[i] = pb[K];
           qcar[i] = qb[K];
           const bool cons = ycons || (i == 0 && xcons0), shared = shy || (i == 0 && shx0);
-          zcolumn(pb, qb, vcar[i], first, last, cons, shared, outl + yown * Nx + K * ccx + i, gzb, chunk);
+          zcolumn(pb, qb, vcar[i], first, last, cons, shared, outl + yown * Nx + K * ccx + i, zm, am);
         }
       }
       if (has_e) {
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
         }
         pcar[K] = pb[K];
         qcar[K] = qb[K];
-        zcolumn(pb, qb, vcar[K], first, last, e_cons, e_sh, outl + ey * Nx + ex, gzb, chunk);
+        zcolumn(pb, qb, vcar[K], first, last, e_cons, e_sh, outl + ey * Nx + ex, zm, am);
       }
     }
     if (next >= nitems) break;
