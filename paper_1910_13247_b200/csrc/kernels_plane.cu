@@ -209,8 +209,13 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
     for (int l = 0; l <= K; ++l) {
       if (l == K && !last) break;  // carried to the next layer
       if (!((zm >> l) & 1u)) {
-        if (shared || ((am >> l) & 1u)) atomicAdd(out, v[l]);
-        else *out = v[l];
+        // predicated red / st, no divergent branch (shared varies across lanes)
+        const int at = (shared || ((am >> l) & 1u)) ? 1 : 0;
+        asm volatile(
+            "{\n .reg .pred pa;\n setp.ne.s32 pa, %2, 0;\n"
+            " @pa red.global.add.f64 [%0], %1;\n @!pa st.global.f64 [%0], %1;\n}\n" ::"l"(out),
+            "d"(v[l]), "r"(at)
+            : "memory");
       }
       out += plane;
     }
