@@ -18,6 +18,7 @@
 // a __grid_constant__ kernel parameter, so every matrix entry is a constant-bank
 // operand of the DFMA.
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -353,6 +354,171 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3D general kernel (the default for dim = 3): the same a3-a7 arithmetic as
+// k_apply_general, reorganised so that a thread keeps ONE pencil index p of one
+// cell for the whole kernel.  Its three pencil slot lists (along x, y, z) are
+// then computed once, the x-pencils are gathered / scattered straight between
+// global memory and registers, and the z-direction steps that follow each other
+// (S_z -> Co_z; q-point operation -> Co_z^T) stay in the registers of the
+// z-pencil that produced them:
+//   1 gather x-pencil, S_x            (regs -> U)
+//   2 S_y                             (U -> U)
+//   3 S_z -> Q (U), Co_z Q -> G2      (regs)
+//   4 Co_x Q -> G0, Co_y Q -> G1
+//   5 q-point op on the z-pencil, t2 -> Co_z^T in regs -> G2
+//   6 Co_x^T G0, Co_y^T G1            (in place)
+//   7 R = G0 + G1 + G2, S_z^T         (-> U)
+//   8 S_y^T
+//   9 S_x^T in regs, scatter-add + identity rows
+template <int K, int GEOM>
+__global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tables t, const __grid_constant__ Geo g,
+                                                     const double *__restrict__ src, double *__restrict__ dst,
+                                                     const double *__restrict__ metric, int cpb) {
+  constexpr int N = K + 1, NP = N * N, NV = NP * N;
+  constexpr int CS = 4 * NV;  // U, G0, G1, G2 per cell
+  extern __shared__ double sm[];
+  const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
+  const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
+  const bool active = cl < cpb;
+  const int64_t cell = (int64_t)blockIdx.x * cpb + cl;
+  const bool valid = active && cell < ncells;
+  double *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV, *G2 = U + 3 * NV;
+  int o0[N], o1[N], o2[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    o0[i] = pen_off<3, N>(0, p, i);
+    o1[i] = pen_off<3, N>(1, p, i);
+    o2[i] = pen_off<3, N>(2, p, i);
+  }
+  const int64_t Nx = g.N[0], plane = g.N[0] * g.N[1];
+  const CellInfo ci = cell_info<3, K>(g, valid ? cell : ncells, ncells);
+  double a[N], b[N];
+
+  // 1: gather the x-pencil (y = p % N, z = p / N), S along x
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      int64_t gi;
+      bool cons, owner;
+      node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
+      a[i] = (valid && !cons) ? __ldg(src + gi) : 0.0;
+    }
+    mat1d<N, false>(t.S, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) U[o0[i]] = b[i];
+  }
+  __syncthreads();
+  // 2: S along y
+  if (active) sweep_inplace<3, N, false>(t.S, U, 1, p);
+  __syncthreads();
+  // 3: S along z -> Q at the Gauss points; Co along z of this z-pencil in registers
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) a[i] = U[o2[i]];
+    mat1d<N, false>(t.S, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) U[o2[i]] = b[i];
+    mat1d<N, false>(t.Co, b, a);
+#pragma unroll
+    for (int i = 0; i < N; ++i) G2[o2[i]] = a[i];
+  }
+  __syncthreads();
+  // 4: Co along x and y of Q
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) a[i] = U[o0[i]];
+    mat1d<N, false>(t.Co, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) G0[o0[i]] = b[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) a[i] = U[o1[i]];
+    mat1d<N, false>(t.Co, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) G1[o1[i]] = b[i];
+  }
+  __syncthreads();
+  // 5: quadrature-point operation on the z-pencil (q = p + NP i), then Co_z^T in registers
+  if (active) {
+    constexpr int NGC = 6;
+    const int qx = p % N, qy = p / N;
+    const double *Gm = metric + (valid ? cell * NV + p : 0);
+    const int64_t cstride = ncells * NV;
+    double t2[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double gr0 = G0[o2[i]], gr1 = G1[o2[i]], gr2 = G2[o2[i]];
+      double tt0, tt1, tt2;
+      if (GEOM == 2) {
+        double G[NGC];
+#pragma unroll
+        for (int c = 0; c < NGC; ++c) G[c] = valid ? __ldg(Gm + c * cstride + NP * i) : 0.0;
+        tt0 = G[0] * gr0 + G[1] * gr1 + G[2] * gr2;
+        tt1 = G[1] * gr0 + G[3] * gr1 + G[4] * gr2;
+        tt2 = G[2] * gr0 + G[4] * gr1 + G[5] * gr2;
+      } else {
+        double W = t.w[qx] * t.w[qy] * t.w[i];
+        if (GEOM == 1) {
+          double x[3];
+          x[0] = g.lo[0] + g.h[0] * ((double)ci.cx + t.xi[qx]);
+          x[1] = g.lo[1] + g.h[1] * ((double)ci.cy + t.xi[qy]);
+          x[2] = g.lo[2] + g.h[2] * ((double)(ci.cz + g.cz0) + t.xi[i]);
+          W *= coeff_var(x, 3) * (g.h[0] * g.h[1] * g.h[2]);
+          tt0 = W / (g.h[0] * g.h[0]) * gr0;
+          tt1 = W / (g.h[1] * g.h[1]) * gr1;
+          tt2 = W / (g.h[2] * g.h[2]) * gr2;
+        } else {
+          tt0 = W * g.fcart[0] * gr0;
+          tt1 = W * g.fcart[1] * gr1;
+          tt2 = W * g.fcart[2] * gr2;
+        }
+      }
+      G0[o2[i]] = tt0;
+      G1[o2[i]] = tt1;
+      t2[i] = tt2;
+    }
+    mat1d<N, true>(t.Co, t2, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) G2[o2[i]] = b[i];
+  }
+  __syncthreads();
+  // 6: Co^T along x of G0, along y of G1
+  if (active) {
+    sweep_inplace<3, N, true>(t.Co, G0, 0, p);
+    sweep_inplace<3, N, true>(t.Co, G1, 1, p);
+  }
+  __syncthreads();
+  // 7: R = G0 + G1 + G2, S^T along z
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) a[i] = G0[o2[i]] + G1[o2[i]] + G2[o2[i]];
+    mat1d<N, true>(t.S, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) U[o2[i]] = b[i];
+  }
+  __syncthreads();
+  // 8: S^T along y
+  if (active) sweep_inplace<3, N, true>(t.S, U, 1, p);
+  __syncthreads();
+  // 9: S^T along x in registers; scatter-add, identity rows by their owner cell
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) a[i] = U[o0[i]];
+    mat1d<N, true>(t.S, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      int64_t gi;
+      bool cons, owner;
+      node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
+      if (cons) {
+        if (owner) dst[gi] = __ldg(src + gi);
+      } else {
+        atomicAdd(dst + gi, b[i]);
+      }
+    }
+  }
+}
+
 template <int DIM, int K>
 static int cells_per_block() {
   constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
@@ -372,6 +538,14 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
   const int64_t blocks = (ncells + cpb - 1) / cpb;
   const size_t smem = (size_t)cpb * ((DIM + 1) * NV * sizeof(double) + sizeof(CellInfo));
   if (blocks == 0) return cudaSuccess;
+  static const bool v1 = std::getenv("MF_GENERAL_V1") != nullptr;  // the original layout (comparisons)
+  if constexpr (DIM == 3) {
+    if (!v1) {
+      k_apply_cell3<K, GEOM><<<(unsigned)blocks, threads, (size_t)cpb * 4 * NV * sizeof(double), s>>>(t, g, src, dst,
+                                                                                                        metric, cpb);
+      return cudaGetLastError();
+    }
+  }
   k_apply_general<DIM, K, GEOM><<<(unsigned)blocks, threads, smem, s>>>(t, g, src, dst, metric, cpb);
   return cudaGetLastError();
 }
