@@ -371,19 +371,77 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
 //   7 R = G0 + G1 + G2, S_z^T         (-> U)
 //   8 S_y^T
 //   9 S_x^T in regs, scatter-add + identity rows
+// cells per block of k_apply_cell3: ~256 threads, ~128 with the staged metric
+// (6 NV doubles per cell of extra shared memory), shared memory <= 48 KB
+template <int K, int GEOM>
+__host__ __device__ constexpr int cell3_cpb() {
+  constexpr int N = K + 1, NP = N * N, NV = NP * N;
+  constexpr int per_cell = 8 * (4 + (GEOM == 2 ? 6 : 0)) * NV;
+  int c = (GEOM == 2 ? 128 : 256) / NP;
+  while (c > 1 && c * per_cell > 48 * 1024) --c;
+  return c < 1 ? 1 : c;
+}
+
 template <int K, int GEOM>
 __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tables t, const __grid_constant__ Geo g,
                                                      const double *__restrict__ src, double *__restrict__ dst,
-                                                     const double *__restrict__ metric, int cpb) {
+                                                     const double *__restrict__ metric) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   constexpr int CS = 4 * NV;  // U, G0, G1, G2 per cell
+  constexpr int cpb = cell3_cpb<K, GEOM>();
   extern __shared__ double sm[];
   const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
   const bool active = cl < cpb;
-  const int64_t cell = (int64_t)blockIdx.x * cpb + cl;
+  const int64_t cell0 = (int64_t)blockIdx.x * cpb, cell = cell0 + cl;
   const bool valid = active && cell < ncells;
   double *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV, *G2 = U + 3 * NV;
+  // curved cells: the block's metric [6][cpb][NV] is staged into shared memory by
+  // cp.async at kernel start, so its HBM latency overlaps steps 1-4
+  double *Ms = sm + cpb * CS;
+  __shared__ alignas(8) unsigned long long mbar;
+  bool bulk = false;
+  if (GEOM == 2) {
+    constexpr int CH = cpb * NV;  // doubles per component chunk
+    const int64_t cstride = ncells * NV;
+    const int64_t rem = ncells - cell0;
+    const int ncb = rem < cpb ? (int)rem : cpb;
+    const unsigned bytes = (unsigned)ncb * NV * 8;
+    // one thread, six bulk copies (TMA engine) completing on an mbarrier; the
+    // 8-byte cp.async loop covers chunks that are not 16-byte multiples
+    bulk = (bytes % 16 == 0) && ((cell0 * NV) % 2 == 0) && (cstride % 2 == 0) &&
+           ((reinterpret_cast<uintptr_t>(metric) & 15) == 0);
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(6 * bytes) : "memory");
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(Ms + c * CH);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(sa),
+              "l"(metric + c * cstride + cell0 * NV), "r"(bytes), "r"(mb)
+              : "memory");
+        }
+      }
+    } else {
+      const int avail = ncb * NV;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const double *gc = metric + c * cstride + cell0 * NV;
+        for (int r = threadIdx.x; r < CH; r += blockDim.x) {
+          const bool ok = r < avail;
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(Ms + c * CH + r);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(ok ? gc + r : metric),
+                       "r"(ok ? 8 : 0)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+  }
   int o0[N], o1[N], o2[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -437,13 +495,23 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
 #pragma unroll
     for (int i = 0; i < N; ++i) G1[o1[i]] = b[i];
   }
+  if (GEOM == 2) {
+    if (bulk) {
+      const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+      asm volatile(
+          "{\n .reg .pred P1;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+          " @!P1 bra WAIT%=;\n}\n" ::"r"(mb)
+          : "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+  }
   __syncthreads();
   // 5: quadrature-point operation on the z-pencil (q = p + NP i), then Co_z^T in registers
   if (active) {
     constexpr int NGC = 6;
     const int qx = p % N, qy = p / N;
-    const double *Gm = metric + (valid ? cell * NV + p : 0);
-    const int64_t cstride = ncells * NV;
+    const double *Gm = Ms + cl * NV + p;
     double t2[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -452,7 +520,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
       if (GEOM == 2) {
         double G[NGC];
 #pragma unroll
-        for (int c = 0; c < NGC; ++c) G[c] = valid ? __ldg(Gm + c * cstride + NP * i) : 0.0;
+        for (int c = 0; c < NGC; ++c) G[c] = Gm[c * cpb * NV + NP * i];
         tt0 = G[0] * gr0 + G[1] * gr1 + G[2] * gr2;
         tt1 = G[1] * gr0 + G[3] * gr1 + G[4] * gr2;
         tt2 = G[2] * gr0 + G[4] * gr1 + G[5] * gr2;
@@ -541,8 +609,10 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
   static const bool v1 = std::getenv("MF_GENERAL_V1") != nullptr;  // the original layout (comparisons)
   if constexpr (DIM == 3) {
     if (!v1) {
-      k_apply_cell3<K, GEOM><<<(unsigned)blocks, threads, (size_t)cpb * 4 * NV * sizeof(double), s>>>(t, g, src, dst,
-                                                                                                        metric, cpb);
+      constexpr int c3 = cell3_cpb<K, GEOM>();
+      const int64_t b3 = (ncells + c3 - 1) / c3;
+      const size_t sm3 = (size_t)c3 * (4 + (GEOM == 2 ? 6 : 0)) * NV * sizeof(double);
+      k_apply_cell3<K, GEOM><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric);
       return cudaGetLastError();
     }
   }
