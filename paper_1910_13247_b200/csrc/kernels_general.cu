@@ -364,11 +364,11 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
 // z-pencil that produced them:
 //   1 gather x-pencil, S_x            (regs -> U)
 //   2 S_y                             (U -> U)
-//   3 S_z -> Q (U), Co_z Q -> G2      (regs)
+//   3 S_z -> Q (U), Co_z Q -> gz      (registers)
 //   4 Co_x Q -> G0, Co_y Q -> G1
-//   5 q-point op on the z-pencil, t2 -> Co_z^T in regs -> G2
+//   5 q-point op on the z-pencil, t_z -> Co_z^T in registers -> gz
 //   6 Co_x^T G0, Co_y^T G1            (in place)
-//   7 R = G0 + G1 + G2, S_z^T         (-> U)
+//   7 R = G0 + G1 + gz, S_z^T         (-> U)
 //   8 S_y^T
 //   9 S_x^T in regs, scatter-add + identity rows
 // cells per block of k_apply_cell3: ~256 threads, ~128 with the staged metric
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
 template <int K, int GEOM>
 __host__ __device__ constexpr int cell3_cpb() {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
-  constexpr int per_cell = 8 * (4 + (GEOM == 2 ? 6 : 0)) * NV;
+  constexpr int per_cell = 8 * (3 + (GEOM == 2 ? 6 : 0)) * NV;
   int c = (GEOM == 2 ? 128 : 256) / NP;
   while (c > 1 && c * per_cell > 48 * 1024) --c;
   return c < 1 ? 1 : c;
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
                                                      const double *__restrict__ src, double *__restrict__ dst,
                                                      const double *__restrict__ metric) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
-  constexpr int CS = 4 * NV;  // U, G0, G1, G2 per cell
+  constexpr int CS = 3 * NV;  // U, G0, G1 per cell (the z-gradient lives in registers)
   constexpr int cpb = cell3_cpb<K, GEOM>();
   extern __shared__ double sm[];
   const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
   const bool active = cl < cpb;
   const int64_t cell0 = (int64_t)blockIdx.x * cpb, cell = cell0 + cl;
   const bool valid = active && cell < ncells;
-  double *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV, *G2 = U + 3 * NV;
+  double *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV;
+  double gz[N];  // z-pencil: Co_z Q (steps 3-5), then Co_z^T t_z (steps 5-7)
   // curved cells: the block's metric [6][cpb][NV] is staged into shared memory by
   // cp.async at kernel start, so its HBM latency overlaps steps 1-4
   double *Ms = sm + cpb * CS;
@@ -477,9 +478,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
     mat1d<N, false>(t.S, a, b);
 #pragma unroll
     for (int i = 0; i < N; ++i) U[o2[i]] = b[i];
-    mat1d<N, false>(t.Co, b, a);
-#pragma unroll
-    for (int i = 0; i < N; ++i) G2[o2[i]] = a[i];
+    mat1d<N, false>(t.Co, b, gz);  // stays in registers until step 5 (same thread, same pencil)
   }
   __syncthreads();
   // 4: Co along x and y of Q
@@ -515,7 +514,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
     double t2[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double gr0 = G0[o2[i]], gr1 = G1[o2[i]], gr2 = G2[o2[i]];
+      const double gr0 = G0[o2[i]], gr1 = G1[o2[i]], gr2 = gz[i];
       double tt0, tt1, tt2;
       if (GEOM == 2) {
         double G[NGC];
@@ -545,9 +544,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
       G1[o2[i]] = tt1;
       t2[i] = tt2;
     }
-    mat1d<N, true>(t.Co, t2, b);
-#pragma unroll
-    for (int i = 0; i < N; ++i) G2[o2[i]] = b[i];
+    mat1d<N, true>(t.Co, t2, gz);  // Co_z^T t2, kept for step 7
   }
   __syncthreads();
   // 6: Co^T along x of G0, along y of G1
@@ -556,10 +553,10 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
     sweep_inplace<3, N, true>(t.Co, G1, 1, p);
   }
   __syncthreads();
-  // 7: R = G0 + G1 + G2, S^T along z
+  // 7: R = G0 + G1 + gz, S^T along z
   if (active) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) a[i] = G0[o2[i]] + G1[o2[i]] + G2[o2[i]];
+    for (int i = 0; i < N; ++i) a[i] = G0[o2[i]] + G1[o2[i]] + gz[i];
     mat1d<N, true>(t.S, a, b);
 #pragma unroll
     for (int i = 0; i < N; ++i) U[o2[i]] = b[i];
@@ -611,7 +608,7 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
     if (!v1) {
       constexpr int c3 = cell3_cpb<K, GEOM>();
       const int64_t b3 = (ncells + c3 - 1) / c3;
-      const size_t sm3 = (size_t)c3 * (4 + (GEOM == 2 ? 6 : 0)) * NV * sizeof(double);
+      const size_t sm3 = (size_t)c3 * (3 + (GEOM == 2 ? 6 : 0)) * NV * sizeof(double);
       k_apply_cell3<K, GEOM><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric);
       return cudaGetLastError();
     }
