@@ -60,9 +60,9 @@ template <int N, bool TR>
 __device__ __forceinline__ void mat1d(const double (&M)[kMaxN][kMaxN], const double *in, double *out) {
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    double s = 0.0;
+    double s = (TR ? M[0][i] : M[i][0]) * in[0];  // = fma(., ., 0.0), one instruction less
 #pragma unroll
-    for (int j = 0; j < N; ++j) s = fma(TR ? M[j][i] : M[i][j], in[j], s);
+    for (int j = 1; j < N; ++j) s = fma(TR ? M[j][i] : M[i][j], in[j], s);
     out[i] = s;
   }
 }
@@ -138,8 +138,19 @@ __device__ __forceinline__ CellInfo cell_info(const Geo &g, int64_t cell, int64_
   ci.base = 0;
   ci.cx = ci.cy = ci.cz = 0;
   if (cell >= ncells) return ci;
-  const int64_t cx = cell % g.nc[0], r = cell / g.nc[0];
-  const int64_t cy = r % g.nc[1], cz = r / g.nc[1];
+  int64_t cx, cy, cz;
+  if (ncells < (int64_t(1) << 31)) {  // 32-bit divisions (every local mesh up to 2^31 cells)
+    const unsigned c = (unsigned)cell, n0 = (unsigned)g.nc[0], n1 = (unsigned)g.nc[1];
+    const unsigned r = c / n0;
+    cx = c - r * n0;
+    cy = r % n1;
+    cz = r / n1;
+  } else {
+    const int64_t r = cell / g.nc[0];
+    cx = cell % g.nc[0];
+    cy = r % g.nc[1];
+    cz = r / g.nc[1];
+  }
   ci.cx = (int)cx;
   ci.cy = (int)cy;
   ci.cz = (int)cz;
