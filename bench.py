@@ -38,6 +38,15 @@ CONFIGS = {
 METRIC = "DoFs/s per matrix-free Laplace apply (3D Q_k FP64)"
 
 
+def load_traffic(config):
+    """ncu-measured DRAM bytes per launch of the timed region (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[config]["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -271,7 +280,7 @@ def main():
                        "apply_variant": info1["apply_variant"],
                        "l2": f"inputs larger than L2: src+dst {16 * n / 1e6:.0f} MB per GPU > 126 MB"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": load_traffic(args.config), "peak_kind": peak_kind,
                          "bytes_per_launch": bytes_per_launch, "kernel_ms": kern_avg_ms,
                          "kernel_share_of_step": kern_avg_ms / ms_per_step},
             "e2e": {"value": e2e_val, "unit": "DoFs/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
