@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -30,6 +31,11 @@ struct mf_op {
   double *h_src = nullptr, *h_dst = nullptr;  // device buffers for mf_apply_host
   double *recv_lo = nullptr, *recv_hi = nullptr;
   ncclComm_t comm = nullptr;
+  // halo overlap (§8(e)): the boundary cell layers first, the NCCL exchange of the shared
+  // planes on comm_stream while the interior layers run on stream
+  bool zsplit = false;  // world > 1, or MF_ZSPLIT=1 (the same launch sequence on one GPU)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   // live kernel timing (mf_set_kernel_timing)
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pairs (start, stop)
@@ -216,7 +222,13 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
     if (cudaMalloc(&op->recv_lo, op->plane * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&op->recv_hi, op->plane * sizeof(double)) != cudaSuccess)
       return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "halo buffers"));
+    if (cudaStreamCreateWithFlags(&op->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&op->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&op->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(fail(MF_ERR_CUDA, "halo stream / events"));
   }
+  const char *zs = std::getenv("MF_ZSPLIT");
+  op->zsplit = world > 1 || (zs && std::atoi(zs) != 0);
   *out = op;
   return MF_OK;
 }
@@ -230,6 +242,9 @@ extern "C" void mf_destroy(mf_op *op) {
   if (op->host_scal) cudaFreeHost(op->host_scal);
   for (cudaEvent_t e : op->ev) cudaEventDestroy(e);
   if (op->comm) ncclCommDestroy(op->comm);
+  if (op->ev_bnd) cudaEventDestroy(op->ev_bnd);
+  if (op->ev_halo) cudaEventDestroy(op->ev_halo);
+  if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
   delete op;
 }
 
@@ -265,25 +280,37 @@ extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
 }
 
 // symmetric exchange of the partial sums on shared z-planes (§8(e)):
-// send my partial of each shared plane, receive the neighbour's, add.
-static mf_status halo_exchange(mf_op *op, double *dst) {
-  if (op->world == 1) return MF_OK;
+// send my partial of each shared plane, receive the neighbour's (on stream s) ...
+static mf_status halo_post(mf_op *op, double *dst, cudaStream_t s) {
   const int64_t np = op->plane;
   double *lo = dst, *hi = dst + op->n_local - np;
   const bool has_lo = op->rank > 0, has_hi = op->rank < op->world - 1;
   NCCL_TRY(ncclGroupStart());
   if (has_hi) {
-    NCCL_TRY(ncclSend(hi, np, ncclDouble, op->rank + 1, op->comm, op->stream));
-    NCCL_TRY(ncclRecv(op->recv_hi, np, ncclDouble, op->rank + 1, op->comm, op->stream));
+    NCCL_TRY(ncclSend(hi, np, ncclDouble, op->rank + 1, op->comm, s));
+    NCCL_TRY(ncclRecv(op->recv_hi, np, ncclDouble, op->rank + 1, op->comm, s));
   }
   if (has_lo) {
-    NCCL_TRY(ncclSend(lo, np, ncclDouble, op->rank - 1, op->comm, op->stream));
-    NCCL_TRY(ncclRecv(op->recv_lo, np, ncclDouble, op->rank - 1, op->comm, op->stream));
+    NCCL_TRY(ncclSend(lo, np, ncclDouble, op->rank - 1, op->comm, s));
+    NCCL_TRY(ncclRecv(op->recv_lo, np, ncclDouble, op->rank - 1, op->comm, s));
   }
   NCCL_TRY(ncclGroupEnd());
-  if (has_hi) CUDA_TRY(launch_plane_add(hi, op->recv_hi, np, op->stream, &op->launches));
-  if (has_lo) CUDA_TRY(launch_plane_add(lo, op->recv_lo, np, op->stream, &op->launches));
   return MF_OK;
+}
+
+// ... and add it (on op->stream; a+b = b+a, so both copies of a shared plane agree bitwise)
+static mf_status halo_add(mf_op *op, double *dst) {
+  const int64_t np = op->plane;
+  double *lo = dst, *hi = dst + op->n_local - np;
+  if (op->rank < op->world - 1) CUDA_TRY(launch_plane_add(hi, op->recv_hi, np, op->stream, &op->launches));
+  if (op->rank > 0) CUDA_TRY(launch_plane_add(lo, op->recv_lo, np, op->stream, &op->launches));
+  return MF_OK;
+}
+
+static mf_status halo_exchange(mf_op *op, double *dst) {
+  if (op->world == 1) return MF_OK;
+  STATUS_TRY(halo_post(op, dst, op->stream));
+  return halo_add(op, dst);
 }
 
 static mf_status timing_mark(mf_op *op) {
@@ -297,8 +324,38 @@ static mf_status timing_mark(mf_op *op) {
   return MF_OK;
 }
 
+// the overlapped apply on z-slabs: part 1 (dst init + the cell layers next to the
+// shared planes), then the NCCL exchange of those planes on comm_stream while part 2
+// (the interior layers, which never touch the shared planes) runs on stream
+static mf_status apply_split(mf_op *op, const double *src, double *dst, int var) {
+  STATUS_TRY(timing_mark(op));
+  if (var == kVariantCartPlane) {
+    CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches, 1));
+  } else {
+    CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
+    CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches, 1));
+  }
+  if (op->world > 1) {
+    CUDA_TRY(cudaEventRecord(op->ev_bnd, op->stream));
+    CUDA_TRY(cudaStreamWaitEvent(op->comm_stream, op->ev_bnd, 0));
+    STATUS_TRY(halo_post(op, dst, op->comm_stream));
+    CUDA_TRY(cudaEventRecord(op->ev_halo, op->comm_stream));
+  }
+  if (var == kVariantCartPlane)
+    CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches, 2));
+  else
+    CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches, 2));
+  STATUS_TRY(timing_mark(op));
+  if (op->world > 1) {
+    CUDA_TRY(cudaStreamWaitEvent(op->stream, op->ev_halo, 0));
+    STATUS_TRY(halo_add(op, dst));
+  }
+  return MF_OK;
+}
+
 static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
   const int var = chosen_variant(op);
+  if (op->zsplit && op->g.dim == 3 && var != kVariantCartTile) return apply_split(op, src, dst, var);
   if (var == kVariantCartTile) {
     STATUS_TRY(timing_mark(op));
     CUDA_TRY(launch_apply_cart_tile(op->g, op->t, src, dst, op->stream, &op->launches));

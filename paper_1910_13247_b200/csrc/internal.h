@@ -54,13 +54,16 @@ enum Variant {
 };
 
 // Kernel launchers (return cudaError_t of the launch).
+// part: 0 = the whole apply; for the halo overlap on z-slabs (§8(e)) 1 = zero dst +
+// the cell layers next to the shared z-planes (first and last), 2 = the interior layers
+// (part 1 then part 2 = part 0).  The 2D and tile paths take part 0 only.
 cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
-                                 const double *metric, cudaStream_t s, int64_t *launches);
+                                 const double *metric, cudaStream_t s, int64_t *launches, int part = 0);
 cudaError_t launch_apply_cart_tile(const Geo &g, const Tables &t, const double *src, double *dst,
                                    cudaStream_t s, int64_t *launches);
 bool cart_tile_supported(const Geo &g);
 cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst,
-                                    cudaStream_t s, int64_t *launches);
+                                    cudaStream_t s, int64_t *launches, int part = 0);
 bool cart_plane_supported(const Geo &g);
 cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
                           int64_t *launches);

@@ -396,7 +396,8 @@ __host__ __device__ constexpr int cell3_cpb() {
 template <int K, int GEOM>
 __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tables t, const __grid_constant__ Geo g,
                                                      const double *__restrict__ src, double *__restrict__ dst,
-                                                     const double *__restrict__ metric) {
+                                                     const double *__restrict__ metric, int64_t cbeg,
+                                                     int64_t cend) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   constexpr int CS = 3 * NV;  // U, G0, G1 per cell (the z-gradient lives in registers)
   constexpr int cpb = cell3_cpb<K, GEOM>();
@@ -404,8 +405,8 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
   const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
   const bool active = cl < cpb;
-  const int64_t cell0 = (int64_t)blockIdx.x * cpb, cell = cell0 + cl;
-  const bool valid = active && cell < ncells;
+  const int64_t cell0 = cbeg + (int64_t)blockIdx.x * cpb, cell = cell0 + cl;  // cells [cbeg, cend)
+  const bool valid = active && cell < cend;
   double *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV;
   double gz[N];  // z-pencil: Co_z Q (steps 3-5), then Co_z^T t_z (steps 5-7)
   // curved cells: the block's metric [6][cpb][NV] is staged into shared memory by
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
   if (GEOM == 2) {
     constexpr int CH = cpb * NV;  // doubles per component chunk
     const int64_t cstride = ncells * NV;
-    const int64_t rem = ncells - cell0;
+    const int64_t rem = cend - cell0;
     const int ncb = rem < cpb ? (int)rem : cpb;
     const unsigned bytes = (unsigned)ncb * NV * 8;
     // one thread, six bulk copies (TMA engine) completing on an mbarrier; the
@@ -604,42 +605,45 @@ static int cells_per_block() {
   return cpb < 1 ? 1 : cpb;
 }
 
+// cells [cbeg, cend) (the 3D kernel; the 2D / v1 kernel always takes every cell)
 template <int DIM, int K, int GEOM>
 static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double *src, double *dst,
-                                    const double *metric, cudaStream_t s) {
+                                    const double *metric, cudaStream_t s, int64_t cbeg, int64_t cend) {
   constexpr int N = K + 1, NP = Shape<DIM, N>::NP, NV = Shape<DIM, N>::NV;
   const int cpb = cells_per_block<DIM, K>();
   int threads = ((cpb * NP + 31) / 32) * 32;
   const int64_t ncells = g.nc[0] * g.nc[1] * (DIM == 3 ? g.nc[2] : 1);
   const int64_t blocks = (ncells + cpb - 1) / cpb;
   const size_t smem = (size_t)cpb * ((DIM + 1) * NV * sizeof(double) + sizeof(CellInfo));
-  if (blocks == 0) return cudaSuccess;
+  if (blocks == 0 || cend <= cbeg) return cudaSuccess;
   static const bool v1 = std::getenv("MF_GENERAL_V1") != nullptr;  // the original layout (comparisons)
   if constexpr (DIM == 3) {
     if (!v1) {
       constexpr int c3 = cell3_cpb<K, GEOM>();
-      const int64_t b3 = (ncells + c3 - 1) / c3;
+      const int64_t b3 = (cend - cbeg + c3 - 1) / c3;
       const size_t sm3 = (size_t)c3 * (3 + (GEOM == 2 ? 6 : 0)) * NV * sizeof(double);
-      k_apply_cell3<K, GEOM><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric);
+      k_apply_cell3<K, GEOM><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric, cbeg,
+                                                                                    cend);
       return cudaGetLastError();
     }
   }
+  if (cbeg != 0 || cend != ncells) return cudaErrorNotSupported;
   k_apply_general<DIM, K, GEOM><<<(unsigned)blocks, threads, smem, s>>>(t, g, src, dst, metric, cpb);
   return cudaGetLastError();
 }
 
 template <int DIM, int GEOM>
 static cudaError_t dispatch_k(const Geo &g, const Tables &t, const double *src, double *dst,
-                              const double *metric, cudaStream_t s) {
+                              const double *metric, cudaStream_t s, int64_t cb, int64_t ce) {
   switch (g.k) {
-    case 1: return launch_general_t<DIM, 1, GEOM>(g, t, src, dst, metric, s);
-    case 2: return launch_general_t<DIM, 2, GEOM>(g, t, src, dst, metric, s);
-    case 3: return launch_general_t<DIM, 3, GEOM>(g, t, src, dst, metric, s);
-    case 4: return launch_general_t<DIM, 4, GEOM>(g, t, src, dst, metric, s);
-    case 5: return launch_general_t<DIM, 5, GEOM>(g, t, src, dst, metric, s);
-    case 6: return launch_general_t<DIM, 6, GEOM>(g, t, src, dst, metric, s);
-    case 7: return launch_general_t<DIM, 7, GEOM>(g, t, src, dst, metric, s);
-    case 8: return launch_general_t<DIM, 8, GEOM>(g, t, src, dst, metric, s);
+    case 1: return launch_general_t<DIM, 1, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 2: return launch_general_t<DIM, 2, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 3: return launch_general_t<DIM, 3, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 4: return launch_general_t<DIM, 4, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 5: return launch_general_t<DIM, 5, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 6: return launch_general_t<DIM, 6, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 7: return launch_general_t<DIM, 7, GEOM>(g, t, src, dst, metric, s, cb, ce);
+    case 8: return launch_general_t<DIM, 8, GEOM>(g, t, src, dst, metric, s, cb, ce);
   }
   return cudaErrorInvalidValue;
 }
@@ -649,18 +653,34 @@ static int geom_kind(const Geo &g) {
   return g.coeff_kind == MF_COEFF_VARIABLE ? 1 : 0;
 }
 
-cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
-                                 const double *metric, cudaStream_t s, int64_t *launches) {
+static cudaError_t general_range(const Geo &g, const Tables &t, const double *src, double *dst,
+                                 const double *metric, cudaStream_t s, int64_t *launches, int64_t cb, int64_t ce) {
+  if (ce <= cb) return cudaSuccess;
   ++*launches;
   const int gk = geom_kind(g);
   if (g.dim == 2) {
-    if (gk == 0) return dispatch_k<2, 0>(g, t, src, dst, metric, s);
-    if (gk == 1) return dispatch_k<2, 1>(g, t, src, dst, metric, s);
-    return dispatch_k<2, 2>(g, t, src, dst, metric, s);
+    if (gk == 0) return dispatch_k<2, 0>(g, t, src, dst, metric, s, cb, ce);
+    if (gk == 1) return dispatch_k<2, 1>(g, t, src, dst, metric, s, cb, ce);
+    return dispatch_k<2, 2>(g, t, src, dst, metric, s, cb, ce);
   }
-  if (gk == 0) return dispatch_k<3, 0>(g, t, src, dst, metric, s);
-  if (gk == 1) return dispatch_k<3, 1>(g, t, src, dst, metric, s);
-  return dispatch_k<3, 2>(g, t, src, dst, metric, s);
+  if (gk == 0) return dispatch_k<3, 0>(g, t, src, dst, metric, s, cb, ce);
+  if (gk == 1) return dispatch_k<3, 1>(g, t, src, dst, metric, s, cb, ce);
+  return dispatch_k<3, 2>(g, t, src, dst, metric, s, cb, ce);
+}
+
+// (the caller zeroes dst before part 0 / part 1)
+cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
+                                 const double *metric, cudaStream_t s, int64_t *launches, int part) {
+  const int64_t layer = g.nc[0] * g.nc[1], ncells = layer * (g.dim == 3 ? g.nc[2] : 1);
+  if (part == 0 || g.dim == 2) return part == 2 ? cudaSuccess : general_range(g, t, src, dst, metric, s, launches, 0, ncells);
+  const int64_t nz = g.nc[2];
+  if (part == 1) {  // the first and the last cell layer (all layers if nz <= 2)
+    if (nz <= 2) return general_range(g, t, src, dst, metric, s, launches, 0, ncells);
+    cudaError_t e = general_range(g, t, src, dst, metric, s, launches, 0, layer);
+    if (e != cudaSuccess) return e;
+    return general_range(g, t, src, dst, metric, s, launches, ncells - layer, ncells);
+  }
+  return nz <= 2 ? cudaSuccess : general_range(g, t, src, dst, metric, s, launches, layer, ncells - layer);
 }
 
 // ---------------------------------------------------------------------------

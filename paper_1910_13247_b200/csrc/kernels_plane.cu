@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   extern __shared__ double sm[];
   double *Us = sm, *Vp = sm + S::STG, *Vq = Vp + S::NV;
 
-  const int ntile = P.ntx * P.nty, nitems = ntile * P.nch;
+  const int ntile = P.ntx * P.nty, nitems = ntile * tile_pass_chunks(P);
   const int Nx = (int)P.Nx, Ny = (int)P.Ny;
   const int64_t plane = P.Nx * P.Ny;
   const uint32_t d = P.dirichlet;
@@ -74,15 +74,14 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   auto item_of = [&](int it) {
     Item I;
     const int tile = it % ntile;
-    I.chunk = it / ntile;
+    I.chunk = tile_pass_chunk(P, it / ntile);
     I.tx = tile % P.ntx;
     I.ty = tile / P.ntx;
     I.cx0 = TX * I.tx;
     I.cy0 = TY * I.ty;
     I.nvx = min(TX, P.ncx - I.cx0);
     I.nvy = min(TY, P.ncy - I.cy0);
-    I.cz_begin = I.chunk * P.LZ;
-    I.cz_end = min(I.cz_begin + P.LZ, P.ncz);
+    tile_chunk_layers(P, I.chunk, I.cz_begin, I.cz_end);
     I.base0 = (int64_t)K * I.cz_begin * plane + (int64_t)K * I.cy0 * P.Nx + (int64_t)K * I.cx0;
     return I;
   };
@@ -353,9 +352,11 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   }
 }
 
+// part 0: init + every chunk; part 1: init + the two boundary chunks of the z-split;
+// part 2: the interior chunks of the z-split (see TileParams::zsplit)
 template <int K, int TX, int TY, bool ISO>
 static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
-                                  int64_t *launches) {
+                                  int64_t *launches, int part) {
   using S = PlaneShape<K, TX, TY>;
   TileParams P;
   tile_params_common(g, t, TX, TY, &P);
@@ -370,11 +371,17 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const double *s
     if (sms < 1) sms = 148;
   }
   const int slots = sms * occ;
-  tile_choose_chunks(&P, slots, 1.0 / K + 0.25);  // the bottom plane costs one extra face per cell
-  cudaError_t e = tile_launch_init(P, g, K, TX, TY, src, dst, s, launches);
-  if (e != cudaSuccess) return e;
+  // the bottom plane costs one extra face per cell
+  if (part == 0) tile_choose_chunks(&P, slots, 1.0 / K + 0.25);
+  else tile_choose_chunks_split(&P, slots, 1.0 / K + 0.25);
+  P.pass = part;
+  if (part != 2) {
+    cudaError_t e = tile_launch_init(P, g, K, TX, TY, src, dst, s, launches);
+    if (e != cudaSuccess) return e;
+  }
+  const int items = P.ntx * P.nty * tile_pass_chunks(P);
+  if (items == 0) return cudaSuccess;
   ++*launches;
-  const int items = P.ntx * P.nty * P.nch;
   const int blocks = std::min(items, slots);
   k_apply_plane<K, TX, TY, ISO><<<blocks, S::NT, S::SMEM, s>>>(P, src, dst);
   return cudaGetLastError();
@@ -383,22 +390,15 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const double *s
 bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }
 
 cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
-                                    int64_t *launches) {
+                                    int64_t *launches, int part) {
   const bool iso = g.fcart[0] == g.fcart[1] && g.fcart[0] == g.fcart[2];
-#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                           \
-  return iso ? launch_plane_t<KK, TXX, TYY, true>(g, t, src, dst, s, launches)  \
-             : launch_plane_t<KK, TXX, TYY, false>(g, t, src, dst, s, launches)
-  static int shape = -1;  // MF_TILE=16x2 selects the wide tile (experiments)
-  if (shape < 0) {
-    const char *e = getenv("MF_TILE");
-    shape = (e && !strcmp(e, "16x2")) ? 1 : 0;
-  }
+#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                                 \
+  return iso ? launch_plane_t<KK, TXX, TYY, true>(g, t, src, dst, s, launches, part)  \
+             : launch_plane_t<KK, TXX, TYY, false>(g, t, src, dst, s, launches, part)
   switch (g.k) {
     case 2: MF_PLANE_LAUNCH(2, 8, 8);
     case 3: MF_PLANE_LAUNCH(3, 8, 4);
-    case 4:
-      if (shape == 1) MF_PLANE_LAUNCH(4, 16, 2);
-      MF_PLANE_LAUNCH(4, 8, 4);
+    case 4: MF_PLANE_LAUNCH(4, 8, 4);
   }
 #undef MF_PLANE_LAUNCH
   return cudaErrorNotSupported;

@@ -29,6 +29,10 @@ struct TileParams {
   int64_t Nx, Ny, Nz;  // local node counts
   int ncx, ncy, ncz;   // local cell counts
   int ntx, nty, nch, LZ;
+  // z-split (multi-GPU overlap): chunk 0 = cell layer 0, chunk nch-1 = layer ncz-1, the
+  // interior layers in chunks of LZ; pass 1 = the two boundary chunks, pass 2 = the rest
+  // (pass 0 = every chunk).  Without zsplit chunk c = layers [c LZ, (c+1) LZ).
+  int zsplit, pass;
   uint32_t dirichlet;
   int skip_top_identity;
   unsigned long long *prof;  // debug counters [2][8] or null
@@ -227,6 +231,48 @@ static inline void tile_choose_chunks(TileParams *P, int slots, double per_chunk
   P->nch = (P->ncz + P->LZ - 1) / P->LZ;
 }
 
+// the z-split chunking: boundary layers alone, the ncz - 2 interior layers balanced
+static inline void tile_choose_chunks_split(TileParams *P, int slots, double per_chunk_overhead) {
+  P->zsplit = 1;
+  if (P->ncz <= 2) {
+    P->LZ = 1;
+    P->nch = P->ncz;  // one or two boundary chunks, no interior
+    return;
+  }
+  TileParams Q = *P;
+  Q.ncz = P->ncz - 2;
+  tile_choose_chunks(&Q, slots, per_chunk_overhead);
+  P->LZ = Q.LZ;
+  P->nch = Q.nch + 2;
+}
+
+// items (tile, chunk) of a pass, and the chunk's cell layers
+__host__ __device__ inline int tile_pass_chunks(const TileParams &P) {
+  if (P.pass == 0) return P.nch;
+  if (P.pass == 1) return P.nch >= 2 ? 2 : 1;
+  return P.nch > 2 ? P.nch - 2 : 0;
+}
+__host__ __device__ inline int tile_pass_chunk(const TileParams &P, int j) {
+  if (P.pass == 0) return j;
+  if (P.pass == 1) return j == 0 ? 0 : P.nch - 1;
+  return 1 + j;
+}
+__host__ __device__ inline void tile_chunk_layers(const TileParams &P, int c, int &b, int &e) {
+  if (!P.zsplit) {
+    b = c * P.LZ;
+    e = b + P.LZ < P.ncz ? b + P.LZ : P.ncz;
+  } else if (c == 0) {
+    b = 0;
+    e = 1;
+  } else if (c == P.nch - 1) {
+    b = P.ncz - 1;
+    e = P.ncz;
+  } else {
+    b = 1 + (c - 1) * P.LZ;
+    e = b + P.LZ < P.ncz - 1 ? b + P.LZ : P.ncz - 1;
+  }
+}
+
 // init kernel: planes shared between blocks (internal tile edges, chunk planes)
 // get 0, Dirichlet faces get the identity value
 static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, int K, int TX, int TY,
@@ -245,7 +291,12 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
   };
   fam(0, (int64_t)K * TX, (int64_t)K * TX, P.ntx - 1);
   fam(1, (int64_t)K * TY, (int64_t)K * TY, P.nty - 1);
-  fam(2, (int64_t)K * P.LZ, (int64_t)K * P.LZ, P.nch - 1);
+  if (!P.zsplit) {
+    fam(2, (int64_t)K * P.LZ, (int64_t)K * P.LZ, P.nch - 1);
+  } else if (P.nch >= 2) {  // bottom planes of chunks 1 .. nch-1
+    fam(2, (int64_t)K, (int64_t)K * P.LZ, P.nch - 2);
+    fam(2, (int64_t)K * (P.ncz - 1), 1, 1);
+  }
   if (g.dirichlet & 1u) fam(0, 0, 1, 1);
   if (g.dirichlet & 2u) fam(0, P.Nx - 1, 1, 1);
   if (g.dirichlet & 4u) fam(1, 0, 1, 1);

@@ -99,6 +99,37 @@ def test_cartesian_variants_match_oracle(case, variant, torch):
     np.testing.assert_array_equal(y[m], x[m])
 
 
+ZSPLIT_CASES = [
+    (dict(dim=3, n_cells=(9, 10, 11), k=2), "plane"),
+    (dict(dim=3, n_cells=(9, 17, 7), k=4, dirichlet=0b011001), "plane"),
+    (dict(dim=3, n_cells=(5, 3, 20), k=4, dirichlet=0), "plane"),
+    (dict(dim=3, n_cells=(4, 4, 1), k=3), "plane"),
+    (dict(dim=3, n_cells=(4, 4, 2), k=3), "plane"),
+    (dict(dim=3, n_cells=(4, 4, 3), k=3), "plane"),
+    (dict(dim=3, n_cells=(6, 5, 7), k=3, geometry="sine", coeff="variable"), "auto"),
+    (dict(dim=3, n_cells=(3, 3, 2), k=5), "auto"),
+    (dict(dim=3, n_cells=(5, 4, 6), k=2, coeff="variable"), "general"),
+    (dict(dim=3, n_cells=(5, 4, 1), k=2), "general"),
+]
+
+
+@pytest.mark.parametrize("case,variant", ZSPLIT_CASES, ids=lambda v: v if isinstance(v, str) else _id(v))
+def test_zsplit_launch_sequence_matches_oracle(case, variant, torch, monkeypatch):
+    # the multi-GPU overlap order (boundary cell layers, then the interior; §8(e)) run on
+    # one GPU without the exchange: MF_ZSPLIT=1
+    monkeypatch.setenv("MF_ZSPLIT", "1")
+    p = oracle_problem(case)
+    A = oracle.CSR(p)
+    op = cuda_operator(case)
+    op.set_variant(variant)
+    for s in (1, 2):
+        x = seeded(A.n, s)
+        y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_l2(y, A @ x) <= CUDA_ORACLE_TOL, (s, rel_l2(y, A @ x))
+    m = oracle.constrained_mask_fast(p)
+    np.testing.assert_array_equal(y[m], x[m])
+
+
 @pytest.mark.parametrize("case", CASES[::2], ids=_id)
 def test_diagonal_matches_assembled_oracle(case, torch):
     p = oracle_problem(case)
