@@ -177,6 +177,53 @@ mf_status mf_set_apply_variant(mf_op *op, int32_t variant);
 mf_status mf_set_kernel_timing(mf_op *op, int32_t enable);
 mf_status mf_kernel_timing(mf_op *op, double *ms_total, int64_t *count);
 
+/* ---- Geometric multigrid (§6.1;
+ * SPEC S:602-695) ------------------------------------------------------------
+ * A hierarchy of globally refined bricks: level L-1 is `finest`, level l has
+ * finest.n_cells / 2^(L-1-l) cells per direction, the same degree, geometry,
+ * coefficient and Dirichlet faces on every level.  Level operators are mf_op's.
+ * Transfer: prolongation = interpolation of the coarse Q_k function at the fine
+ * GLL support points (tensor product of 1D interpolations), restriction = its
+ * exact transpose; constrained DoFs are 0 on every level.  Smoother: the
+ * Chebyshev(degree) polynomial of mf_chebyshev on [lam_l/range, lam_l],
+ * lam_l = safety * Ritz(eig_steps) of the level (pre: x = Cheb(b); post:
+ * x += Cheb(b - A x)).  Coarse solver: the dense inverse of level 0 (built once on
+ * the GPU by Gauss-Jordan elimination), so one V-cycle is a fixed symmetric linear
+ * operator.  Single GPU (world_size 1).  Ownership: the hierarchy owns its level
+ * ops and scratch vectors; every vector argument is a caller-owned device buffer
+ * of the stated level's n_local doubles. */
+typedef struct mf_mg mf_mg; /* opaque */
+typedef struct {
+  int32_t n_levels;        /* 0: halve while every direction is even and the coarser level has > max_coarse_dofs DoFs */
+  int64_t max_coarse_dofs; /* e.g. 1000; MF_ERR_ARGUMENT if the coarse level would exceed 8192 DoFs */
+  int32_t smooth_degree;   /* Chebyshev degree of pre- and post-smoothing, 6 */
+  double smooth_range;     /* 20 */
+  double smooth_safety;    /* 1.2 */
+  int32_t eig_cg_steps;    /* 12 */
+} mf_mg_params;
+/* Errors: MF_ERR_ARGUMENT (n_cells not divisible by 2^(levels-1), bad parameters),
+ * plus every error of mf_create. */
+mf_status mf_mg_create(const mf_mesh *finest, int32_t degree, const mf_coeff *coeff, const mf_mg_params *params,
+                       mf_mg **out);
+void mf_mg_destroy(mf_mg *mg);
+/* number of levels; n_local of level l (0 = coarsest); the level's operator
+ * (borrowed, valid until mf_mg_destroy); lambda_l (with the safety factor) */
+mf_status mf_mg_levels(const mf_mg *mg, int32_t *n_levels);
+mf_status mf_mg_level_size(const mf_mg *mg, int32_t level, int64_t *n_local);
+mf_status mf_mg_level_op(mf_mg *mg, int32_t level, mf_op **op);
+mf_status mf_mg_level_lambda(const mf_mg *mg, int32_t level, double *lambda);
+/* fine(level) = P coarse(level - 1); coarse(level - 1) = P^T fine(level); 1 <= level < L.  Asynchronous. */
+mf_status mf_mg_prolongate(mf_mg *mg, int32_t level, const double *coarse, double *fine);
+mf_status mf_mg_restrict(mf_mg *mg, int32_t level, const double *fine, double *coarse);
+/* x = V(b): one V-cycle on the finest level, from x = 0.  Asynchronous, no host syncs. */
+mf_status mf_mg_vcycle(mf_mg *mg, const double *b, double *x, int64_t n);
+/* CG on the finest level with one V-cycle as preconditioner; same
+ * stopping rule, history and errors as mf_cg_solve (result->lambda_max = lambda of
+ * the finest level).  Blocks. */
+mf_status mf_mg_cg_solve(mf_mg *mg, const double *b, double *x, int64_t n, double rel_tol, int32_t max_iter,
+                         mf_cg_result *result, double *history, int32_t history_cap);
+mf_status mf_mg_set_stream(mf_mg *mg, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

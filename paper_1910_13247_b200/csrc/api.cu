@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -70,6 +71,7 @@ static mf_status fail(mf_status s, const std::string &msg) {
   } while (0)
 
 extern "C" const char *mf_last_error(void) { return g_err.c_str(); }
+mf_status mf_set_error(mf_status s, const std::string &msg) { return fail(s, msg); }
 
 extern "C" mf_status mf_nccl_unique_id(uint8_t *out128) {
   if (!out128) return fail(MF_ERR_ARGUMENT, "null output");
@@ -553,29 +555,18 @@ extern "C" mf_status mf_chebyshev(mf_op *op, const double *r, double *z, int64_t
   return cheb_impl(op, r, z, lambda, degree, smoothing_range);
 }
 
-// O9 / S:500-508: PCG from x0 = 0 with P = Chebyshev(cheb_degree) (or Jacobi if 0)
-extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t n, const mf_cg_params *prm,
-                                 mf_cg_result *res, double *history, int32_t history_cap) {
-  if (!op || !b || !x || !prm || !res) return fail(MF_ERR_ARGUMENT, "null argument");
-  if (n != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
-  if (!(prm->rel_tol > 0.0) || prm->max_iter < 1) return fail(MF_ERR_ARGUMENT, "bad CG parameters");
+// O9 / S:500-508: PCG from x0 = 0 with the preconditioner z = precond(r) (device
+// buffers of n_local); stopping rule, history and errors of mf_cg_solve.  Also the
+// outer loop of the multigrid solver (mg.cu).
+mf_status cg_core(mf_op *op, const double *b, double *x, double rel_tol, int max_iter,
+                  const std::function<mf_status(const double *, double *)> &precond, mf_cg_result *res,
+                  double *history, int32_t history_cap) {
   STATUS_TRY(ensure_solver(op));
+  const int64_t n = op->n_local;
   cudaStream_t s = op->stream;
   double *r = op->r, *p = op->p, *v = op->v, *z = op->z;
   res->iterations = 0;
   res->final_rel_residual = 0.0;
-  res->lambda_max = 0.0;
-  double lam = 0.0;
-  if (prm->cheb_degree > 0) {
-    STATUS_TRY(lambda_impl(op, prm->eig_cg_steps, &lam));
-    lam *= prm->cheb_safety;
-    res->lambda_max = lam;
-  }
-  auto precond = [&](const double *rr, double *zz) -> mf_status {
-    if (prm->cheb_degree > 0) return cheb_impl(op, rr, zz, lam, prm->cheb_degree, prm->cheb_range);
-    CUDA_TRY(launch_mul(op->dinv, rr, zz, n, s, &op->launches));
-    return MF_OK;
-  };
   CUDA_TRY(launch_zero(x, n, s, &op->launches));
   CUDA_TRY(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   {
@@ -615,8 +606,8 @@ extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t 
     if (history && it <= history_cap) history[it - 1] = resn;
     res->iterations = it;
     res->final_rel_residual = resn / normb;
-    if (resn <= prm->rel_tol * normb) return MF_OK;
-    if (it >= prm->max_iter) return fail(MF_ERR_MAX_ITERATIONS, "CG did not converge");
+    if (resn <= rel_tol * normb) return MF_OK;
+    if (it >= max_iter) return fail(MF_ERR_MAX_ITERATIONS, "CG did not converge");
     STATUS_TRY(precond(r, z));
     {
       const double *a[1] = {r}, *bb[1] = {z};
@@ -629,6 +620,30 @@ extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t 
     CUDA_TRY(launch_cg_update_p(op->dev_scal + 5, z, p, n, s, &op->launches));
     rz = rzn;
   }
+}
+
+// Chebyshev(cheb_degree)-Jacobi PCG (or plain Jacobi if 0)
+extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t n, const mf_cg_params *prm,
+                                 mf_cg_result *res, double *history, int32_t history_cap) {
+  if (!op || !b || !x || !prm || !res) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  if (!(prm->rel_tol > 0.0) || prm->max_iter < 1) return fail(MF_ERR_ARGUMENT, "bad CG parameters");
+  STATUS_TRY(ensure_solver(op));
+  res->iterations = 0;
+  res->final_rel_residual = 0.0;
+  res->lambda_max = 0.0;
+  double lam = 0.0;
+  if (prm->cheb_degree > 0) {
+    STATUS_TRY(lambda_impl(op, prm->eig_cg_steps, &lam));
+    lam *= prm->cheb_safety;
+    res->lambda_max = lam;
+  }
+  auto precond = [&](const double *rr, double *zz) -> mf_status {
+    if (prm->cheb_degree > 0) return cheb_impl(op, rr, zz, lam, prm->cheb_degree, prm->cheb_range);
+    CUDA_TRY(launch_mul(op->dinv, rr, zz, n, op->stream, &op->launches));
+    return MF_OK;
+  };
+  return cg_core(op, b, x, prm->rel_tol, prm->max_iter, precond, res, history, history_cap);
 }
 
 extern "C" mf_status mf_get_info(const mf_op *op, mf_info *info) {

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <functional>
 #include <string>
 
 #include "../../include/mf.h"
@@ -100,3 +101,9 @@ cudaError_t launch_plane_add(double *dst, const double *recv, int64_t n, cudaStr
 constexpr int kDotBlocks = 592;  // 4 x 148 SMs
 
 }  // namespace mf
+
+// api.cu internals shared with mg.cu (C++ linkage, not part of the C ABI)
+mf_status cg_core(mf_op *op, const double *b, double *x, double rel_tol, int max_iter,
+                  const std::function<mf_status(const double *, double *)> &precond, mf_cg_result *res,
+                  double *history, int32_t history_cap);
+mf_status mf_set_error(mf_status s, const std::string &msg);  // sets mf_last_error, returns s

@@ -54,6 +54,11 @@ class CGResultC(ctypes.Structure):
                 ("lambda_max", ctypes.c_double)]
 
 
+class MGParams(ctypes.Structure):
+    _fields_ = [("n_levels", ctypes.c_int32), ("max_coarse_dofs", ctypes.c_int64), ("smooth_degree", ctypes.c_int32),
+                ("smooth_range", ctypes.c_double), ("smooth_safety", ctypes.c_double), ("eig_cg_steps", ctypes.c_int32)]
+
+
 class Info(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("degree", ctypes.c_int32), ("geometry", ctypes.c_int32),
                 ("coeff_kind", ctypes.c_int32), ("apply_variant", ctypes.c_int32),
@@ -64,7 +69,9 @@ class Info(ctypes.Structure):
 EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_sizes", "mf_set_stream",
            "mf_apply", "mf_apply_host", "mf_diagonal", "mf_estimate_lambda_max", "mf_chebyshev",
            "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing",
-           "mf_partition"]
+           "mf_partition", "mf_mg_create", "mf_mg_destroy", "mf_mg_levels", "mf_mg_level_size", "mf_mg_level_op",
+           "mf_mg_level_lambda", "mf_mg_prolongate", "mf_mg_restrict", "mf_mg_vcycle", "mf_mg_cg_solve",
+           "mf_mg_set_stream"]
 
 _lib = None
 
@@ -100,6 +107,18 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "mf_nccl_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
         "mf_partition": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                          i64p, i64p, i64p, i64p, i64p, i64p],
+        "mf_mg_create": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.POINTER(Coeff), ctypes.POINTER(MGParams),
+                         ctypes.POINTER(vp)],
+        "mf_mg_levels": [vp, ctypes.POINTER(ctypes.c_int32)],
+        "mf_mg_level_size": [vp, ctypes.c_int32, i64p],
+        "mf_mg_level_op": [vp, ctypes.c_int32, ctypes.POINTER(vp)],
+        "mf_mg_level_lambda": [vp, ctypes.c_int32, dp],
+        "mf_mg_prolongate": [vp, ctypes.c_int32, vp, vp],
+        "mf_mg_restrict": [vp, ctypes.c_int32, vp, vp],
+        "mf_mg_vcycle": [vp, vp, vp, i64],
+        "mf_mg_cg_solve": [vp, vp, vp, i64, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(CGResultC), dp,
+                           ctypes.c_int32],
+        "mf_mg_set_stream": [vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -107,6 +126,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         f.restype = ctypes.c_int
     L.mf_destroy.argtypes = [vp]
     L.mf_destroy.restype = None
+    L.mf_mg_destroy.argtypes = [vp]
+    L.mf_mg_destroy.restype = None
     L.mf_last_error.argtypes = []
     L.mf_last_error.restype = ctypes.c_char_p
     _lib = L
@@ -299,3 +320,101 @@ class Operator:
         ms, n = ctypes.c_double(), ctypes.c_int64()
         _check(load().mf_kernel_timing(self._h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+
+class Multigrid:
+    """Geometric multigrid on the globally refined brick (include/mf.h, mf_mg_*):
+    level l = 0 (coarsest) .. n_levels - 1 (the given mesh); V-cycle with
+    Chebyshev(smooth_degree) smoothing and a dense coarse solve; MG-preconditioned CG."""
+
+    def __init__(self, n_cells, degree, lower=None, upper=None, geometry="cartesian", eps=0.1, coeff=1.0,
+                 dirichlet_faces=None, n_levels=0, max_coarse_dofs=1000, smooth_degree=6, smooth_range=20.0,
+                 smooth_safety=1.2, eig_cg_steps=12):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1910_13247_b200 needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        m = make_mesh(n_cells, 3, lower, upper, geometry, eps, dirichlet_faces)
+        c = Coeff()
+        c.kind, c.value = (1, 0.0) if coeff == "variable" else (0, float(coeff))
+        prm = MGParams(n_levels, max_coarse_dofs, smooth_degree, smooth_range, smooth_safety, eig_cg_steps)
+        h = ctypes.c_void_p()
+        L = load()
+        _check(L.mf_mg_create(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(prm), ctypes.byref(h)))
+        self._h = h
+        nl = ctypes.c_int32()
+        _check(L.mf_mg_levels(h, ctypes.byref(nl)))
+        self.n_levels = nl.value
+        self.sizes = []
+        for l in range(self.n_levels):
+            n = ctypes.c_int64()
+            _check(L.mf_mg_level_size(h, l, ctypes.byref(n)))
+            self.sizes.append(n.value)
+        self.n_local = self.sizes[-1]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().mf_mg_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _stream(self):
+        _check(load().mf_mg_set_stream(self._h, ctypes.c_void_p(self._torch.cuda.current_stream(self.device).cuda_stream)))
+
+    def _vec(self, x, n, name):
+        t = self._torch
+        if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float64 and x.is_contiguous() and x.numel() == n):
+            raise TypeError(f"{name} must be a contiguous float64 CUDA tensor of {n} entries")
+        return ctypes.c_void_p(x.data_ptr())
+
+    def new_vector(self, level=None):
+        n = self.sizes[-1 if level is None else level]
+        return self._torch.zeros(n, dtype=self._torch.float64, device=self.device)
+
+    def level_lambda(self, level: int) -> float:
+        v = ctypes.c_double()
+        _check(load().mf_mg_level_lambda(self._h, level, ctypes.byref(v)))
+        return v.value
+
+    def level_apply(self, level: int, x, out=None):
+        out = self.new_vector(level) if out is None else out
+        op = ctypes.c_void_p()
+        _check(load().mf_mg_level_op(self._h, level, ctypes.byref(op)))
+        self._stream()
+        n = self.sizes[level]
+        _check(load().mf_apply(op, self._vec(x, n, "x"), n, self._vec(out, n, "out"), n))
+        return out
+
+    def prolongate(self, level: int, coarse, out=None):
+        out = self.new_vector(level) if out is None else out
+        self._stream()
+        _check(load().mf_mg_prolongate(self._h, level, self._vec(coarse, self.sizes[level - 1], "coarse"),
+                                       self._vec(out, self.sizes[level], "fine")))
+        return out
+
+    def restrict(self, level: int, fine, out=None):
+        out = self.new_vector(level - 1) if out is None else out
+        self._stream()
+        _check(load().mf_mg_restrict(self._h, level, self._vec(fine, self.sizes[level], "fine"),
+                                     self._vec(out, self.sizes[level - 1], "coarse")))
+        return out
+
+    def vcycle(self, b, out=None):
+        out = self.new_vector() if out is None else out
+        self._stream()
+        _check(load().mf_mg_vcycle(self._h, self._vec(b, self.n_local, "b"), self._vec(out, self.n_local, "x"),
+                                   self.n_local))
+        return out
+
+    def cg_solve(self, b, x=None, rel_tol=1e-10, max_iter=1000, history_cap=2000):
+        x = self.new_vector() if x is None else x
+        r = CGResultC()
+        hist = np.zeros(history_cap)
+        self._stream()
+        _check(load().mf_mg_cg_solve(self._h, self._vec(b, self.n_local, "b"), self._vec(x, self.n_local, "x"),
+                                     self.n_local, rel_tol, max_iter, ctypes.byref(r),
+                                     hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), history_cap))
+        return x, CGResult(r.iterations, r.final_rel_residual, r.lambda_max, hist[:r.iterations].copy())
