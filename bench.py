@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solve", action="store_true", help="also time one Chebyshev(6)-PCG solve")
+    ap.add_argument("--solve-mg", action="store_true", help="also time one multigrid-preconditioned CG solve (1 GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -259,6 +260,7 @@ def main():
     ok = bool(torch.equal(dst[:op.mesh.n_cells[0] * k + 1], src[:op.mesh.n_cells[0] * k + 1])) if rank == 0 else True
 
     solve = None
+    solve_mg = None
     if args.solve:
         b = torch.ones(n, dtype=torch.float64, device="cuda")
         barrier()
@@ -266,6 +268,30 @@ def main():
         x, res = op.cg_solve(b, rel_tol=1e-10)
         barrier()
         solve = {"iterations": res.iterations, "seconds": time.perf_counter() - t0, "lambda_max": res.lambda_max}
+    if args.solve_mg and world == 1:
+        from paper_1910_13247_b200 import Multigrid
+
+        b = torch.ones(n, dtype=torch.float64, device="cuda")
+        t0 = time.perf_counter()
+        M = Multigrid(nc, k, geometry=geom, coeff=coeff)
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter() - t0
+        M.cg_solve(b, rel_tol=1e-10)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, res = M.cg_solve(b, rel_tol=1e-10)
+        torch.cuda.synchronize()
+        t_solve = time.perf_counter() - t0
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(5):
+            M.vcycle(b, x)
+        ev1.record()
+        torch.cuda.synchronize()
+        solve_mg = {"levels": M.n_levels, "level_sizes": M.sizes, "iterations": res.iterations,
+                    "final_rel_residual": res.final_rel_residual, "seconds": t_solve, "setup_seconds": t_setup,
+                    "vcycle_ms": ev0.elapsed_time(ev1) / 5}
+        M.close()
 
     if rank == 0:
         peak, peak_kind = load_peaks()
@@ -291,6 +317,8 @@ def main():
         }
         if solve:
             out["solve"] = solve
+        if solve_mg:
+            out["solve_mg"] = solve_mg
         if not args.no_cpu_baseline and world == 1:
             v, nd, reps, el, t_asm, cores = cpu_baseline_sample(k, geom, coeff)
             out["cpu_baseline"] = {"value": v, "unit": "DoFs/s", "cores": cores, "kind": "oracle",
