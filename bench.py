@@ -272,26 +272,28 @@ def main():
         from paper_1910_13247_b200 import Multigrid
 
         b = torch.ones(n, dtype=torch.float64, device="cuda")
-        t0 = time.perf_counter()
-        M = Multigrid(nc, k, geometry=geom, coeff=coeff)
-        torch.cuda.synchronize()
-        t_setup = time.perf_counter() - t0
-        M.cg_solve(b, rel_tol=1e-10)  # warm-up
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        x, res = M.cg_solve(b, rel_tol=1e-10)
-        torch.cuda.synchronize()
-        t_solve = time.perf_counter() - t0
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for _ in range(5):
-            M.vcycle(b, x)
-        ev1.record()
-        torch.cuda.synchronize()
-        solve_mg = {"levels": M.n_levels, "level_sizes": M.sizes, "iterations": res.iterations,
-                    "final_rel_residual": res.final_rel_residual, "seconds": t_solve, "setup_seconds": t_setup,
-                    "vcycle_ms": ev0.elapsed_time(ev1) / 5}
-        M.close()
+        solve_mg = {}
+        for prec in ("fp64", "mixed"):  # mixed: FP32 V-cycle in the FP64 CG (§8(f) f2)
+            t0 = time.perf_counter()
+            M = Multigrid(nc, k, geometry=geom, coeff=coeff, precision=prec)
+            torch.cuda.synchronize()
+            t_setup = time.perf_counter() - t0
+            M.cg_solve(b, rel_tol=1e-10)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            x, res = M.cg_solve(b, rel_tol=1e-10)
+            torch.cuda.synchronize()
+            t_solve = time.perf_counter() - t0
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(5):
+                M.vcycle(b, x)
+            ev1.record()
+            torch.cuda.synchronize()
+            solve_mg[prec] = {"levels": M.n_levels, "level_sizes": M.sizes, "iterations": res.iterations,
+                              "final_rel_residual": res.final_rel_residual, "seconds": t_solve,
+                              "setup_seconds": t_setup, "vcycle_ms": ev0.elapsed_time(ev1) / 5}
+            M.close()
 
     if rank == 0:
         peak, peak_kind = load_peaks()

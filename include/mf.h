@@ -119,6 +119,12 @@ mf_status mf_apply(mf_op *op, const double *src, int64_t n_src, double *dst, int
 mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_src, double *dst_host,
                         int64_t n_dst);
 
+/* The same operator evaluated in FP32 (device buffers of n_local floats): the FP32
+ * instances of the apply kernels used by the mixed-precision multigrid (SURVEY
+ * §8(f) f2).  3D, world_size 1 only (else MF_ERR_ARGUMENT).
+ * Asynchronous. */
+mf_status mf_apply_f32(mf_op *op, const float *src, int64_t n_src, float *dst, int64_t n_dst);
+
 /* diag = diagonal of A (§8(a) a9), 1 on constrained DoFs.  Asynchronous. */
 mf_status mf_diagonal(mf_op *op, double *diag, int64_t n);
 
@@ -200,6 +206,10 @@ typedef struct {
   double smooth_range;     /* 20 */
   double smooth_safety;    /* 1.2 */
   int32_t eig_cg_steps;    /* 12 */
+  int32_t precision;       /* 0: FP64 V-cycle; 1: FP32 V-cycle (level operators, smoothers, transfers and
+                              coarse solve in single precision) inside the FP64 CG -- the paper's production
+                              setting, "run in single precision ... with some double-precision
+                              correction" */
 } mf_mg_params;
 /* Errors: MF_ERR_ARGUMENT (n_cells not divisible by 2^(levels-1), bad parameters),
  * plus every error of mf_create. */

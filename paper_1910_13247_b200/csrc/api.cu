@@ -28,6 +28,8 @@ struct mf_op {
   // solver scratch (lazily allocated, n_local each)
   double *diag = nullptr, *dinv = nullptr;
   double *r = nullptr, *p = nullptr, *v = nullptr, *z = nullptr, *cd = nullptr, *cax = nullptr;
+  // FP32 copies / scratch for the mixed-precision multigrid (lazily allocated)
+  float *metric_f = nullptr, *dinv_f = nullptr, *cd_f = nullptr, *cax_f = nullptr;
   double *partials = nullptr, *dev_scal = nullptr, *host_scal = nullptr;
   double *h_src = nullptr, *h_dst = nullptr;  // device buffers for mf_apply_host
   double *recv_lo = nullptr, *recv_hi = nullptr;
@@ -238,6 +240,7 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
 extern "C" void mf_destroy(mf_op *op) {
   if (!op) return;
   cudaFree(op->metric);
+  for (float *b : {op->metric_f, op->dinv_f, op->cd_f, op->cax_f}) cudaFree(b);
   for (double *b : {op->diag, op->dinv, op->r, op->p, op->v, op->z, op->cd, op->cax, op->partials, op->dev_scal,
                     op->h_src, op->h_dst, op->recv_lo, op->recv_hi})
     cudaFree(b);
@@ -553,6 +556,61 @@ extern "C" mf_status mf_chebyshev(mf_op *op, const double *r, double *z, int64_t
   if (n != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
   if (degree < 1 || !(lambda > 0.0) || !(smoothing_range > 1.0)) return fail(MF_ERR_ARGUMENT, "bad parameters");
   return cheb_impl(op, r, z, lambda, degree, smoothing_range);
+}
+
+// ---- FP32 operator (mixed-precision multigrid, §8(f) f2; "run in single
+// precision ... combined with some double-precision correction") ----------------
+static mf_status ensure_f32(mf_op *op) {
+  if (op->cd_f) return MF_OK;
+  STATUS_TRY(ensure_solver(op));
+  const int64_t n = op->n_local;
+  CUDA_TRY(cudaMalloc(&op->dinv_f, n * sizeof(float)));
+  CUDA_TRY(cudaMalloc(&op->cd_f, n * sizeof(float)));
+  CUDA_TRY(cudaMalloc(&op->cax_f, n * sizeof(float)));
+  CUDA_TRY(launch_d2f(op->dinv, op->dinv_f, n, op->stream, &op->launches));
+  if (op->metric) {
+    const int64_t nm = (int64_t)ncomp(op->g.dim) * ncells_local(op->g) * ipow(op->g.k + 1, op->g.dim);
+    CUDA_TRY(cudaMalloc(&op->metric_f, nm * sizeof(float)));
+    CUDA_TRY(launch_d2f(op->metric, op->metric_f, nm, op->stream, &op->launches));
+  }
+  return MF_OK;
+}
+
+mf_status apply_f32(mf_op *op, const float *src, float *dst) {
+  if (op->world != 1 || op->g.dim != 3) return fail(MF_ERR_ARGUMENT, "FP32 apply: 3D, one rank");
+  STATUS_TRY(ensure_f32(op));
+  if (chosen_variant(op) == kVariantCartPlane) {
+    CUDA_TRY(launch_apply_cart_plane_f32(op->g, op->t, src, dst, op->stream, &op->launches));
+  } else {
+    CUDA_TRY(launch_zero_f(dst, op->n_local, op->stream, &op->launches));
+    CUDA_TRY(launch_apply_general_f32(op->g, op->t, src, dst, op->metric_f, op->stream, &op->launches));
+  }
+  return MF_OK;
+}
+
+// the Chebyshev polynomial of cheb_impl in FP32 (coefficients rounded from FP64)
+mf_status cheb_f32(mf_op *op, const float *r, float *x, double lam, int degree, double range) {
+  STATUS_TRY(ensure_f32(op));
+  const int64_t n = op->n_local;
+  const double a = lam / range, b = lam;
+  const double theta = 0.5 * (a + b), delta = 0.5 * (b - a), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  CUDA_TRY(launch_cheb_init_f(r, op->dinv_f, (float)(1.0 / theta), x, op->cd_f, n, op->stream, &op->launches));
+  for (int j = 1; j < degree; ++j) {
+    const double rho_n = 1.0 / (2.0 * sigma - rho);
+    STATUS_TRY(apply_f32(op, x, op->cax_f));
+    CUDA_TRY(launch_cheb_step_f(r, op->cax_f, op->dinv_f, (float)(rho_n * rho), (float)(2.0 * rho_n / delta), x,
+                                op->cd_f, n, op->stream, &op->launches));
+    rho = rho_n;
+  }
+  return MF_OK;
+}
+
+extern "C" mf_status mf_apply_f32(mf_op *op, const float *src, int64_t n_src, float *dst, int64_t n_dst) {
+  if (!op || !src || !dst) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n_src != op->n_local || n_dst != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  if ((const void *)src == (const void *)dst) return fail(MF_ERR_ARGUMENT, "src and dst must be distinct");
+  return apply_f32(op, src, dst);
 }
 
 // O9 / S:500-508: PCG from x0 = 0 with the preconditioner z = precond(r) (device

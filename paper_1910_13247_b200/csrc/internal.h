@@ -65,6 +65,12 @@ cudaError_t launch_apply_cart_tile(const Geo &g, const Tables &t, const double *
 bool cart_tile_supported(const Geo &g);
 cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst,
                                     cudaStream_t s, int64_t *launches, int part = 0);
+// FP32 versions for the mixed-precision multigrid (§8(f) f2): the same kernels
+// instantiated for float (dst zeroed by the caller for the general kernel)
+cudaError_t launch_apply_cart_plane_f32(const Geo &g, const Tables &t, const float *src, float *dst,
+                                        cudaStream_t s, int64_t *launches);
+cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float *src, float *dst,
+                                     const float *metric, cudaStream_t s, int64_t *launches);
 bool cart_plane_supported(const Geo &g);
 cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
                           int64_t *launches);
@@ -98,6 +104,15 @@ cudaError_t launch_mul(const double *a, const double *b, double *out, int64_t n,
 cudaError_t launch_recip(const double *x, double *y, int64_t n, cudaStream_t s, int64_t *launches);
 cudaError_t launch_plane_add(double *dst, const double *recv, int64_t n, cudaStream_t s, int64_t *launches);
 
+// FP32 vector kernels (mixed-precision multigrid)
+cudaError_t launch_zero_f(float *x, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_d2f(const double *x, float *y, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_f2d(const float *x, double *y, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_cheb_init_f(const float *r, const float *dinv, float c0, float *x, float *d, int64_t n,
+                               cudaStream_t s, int64_t *launches);
+cudaError_t launch_cheb_step_f(const float *r, const float *ax, const float *dinv, float c1, float c2, float *x,
+                               float *d, int64_t n, cudaStream_t s, int64_t *launches);
+
 constexpr int kDotBlocks = 592;  // 4 x 148 SMs
 
 }  // namespace mf
@@ -107,3 +122,6 @@ mf_status cg_core(mf_op *op, const double *b, double *x, double rel_tol, int max
                   const std::function<mf_status(const double *, double *)> &precond, mf_cg_result *res,
                   double *history, int32_t history_cap);
 mf_status mf_set_error(mf_status s, const std::string &msg);  // sets mf_last_error, returns s
+// FP32 operator and Chebyshev polynomial of an op (3D, one rank)
+mf_status apply_f32(mf_op *op, const float *src, float *dst);
+mf_status cheb_f32(mf_op *op, const float *r, float *x, double lam, int degree, double range);

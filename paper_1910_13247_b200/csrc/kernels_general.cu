@@ -56,20 +56,20 @@ __device__ __forceinline__ int nidx(int i) {
 }
 
 // out[i] = sum_j M[i][j] in[j]   (TR: sum_j M[j][i] in[j])
-template <int N, bool TR>
-__device__ __forceinline__ void mat1d(const double (&M)[kMaxN][kMaxN], const double *in, double *out) {
+template <int N, bool TR, class T>
+__device__ __forceinline__ void mat1d(const T (&M)[kMaxN][kMaxN], const T *in, T *out) {
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    double s = (TR ? M[0][i] : M[i][0]) * in[0];  // = fma(., ., 0.0), one instruction less
+    T s = (TR ? M[0][i] : M[i][0]) * in[0];  // = fma(., ., 0.0), one instruction less
 #pragma unroll
     for (int j = 1; j < N; ++j) s = fma(TR ? M[j][i] : M[i][j], in[j], s);
     out[i] = s;
   }
 }
 
-template <int DIM, int N, bool TR>
-__device__ __forceinline__ void sweep_inplace(const double (&M)[kMaxN][kMaxN], double *U, int dir, int p) {
-  double a[N], b[N];
+template <int DIM, int N, bool TR, class T>
+__device__ __forceinline__ void sweep_inplace(const T (&M)[kMaxN][kMaxN], T *U, int dir, int p) {
+  T a[N], b[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) a[i] = U[pen_off<DIM, N>(dir, p, i)];
   mat1d<N, TR>(M, a, b);
@@ -115,6 +115,29 @@ __device__ __forceinline__ bool owner_of(const Geo &g, const CellIdx &ci, int i,
   bool own = (l0 >= 1 || ci.c[0] == 0) && (l1 >= 1 || ci.c[1] == 0) && (DIM == 2 || l2 >= 1 || ci.c[2] == 0);
   if (g.skip_top_identity && DIM == 3 && m[2] == g.N[2] - 1) own = false;
   return own;
+}
+
+// the 1D tables the cell kernels read, in FP32 (mixed-precision multigrid, §8(f) f2)
+struct TablesF {
+  float S[kMaxN][kMaxN];
+  float Co[kMaxN][kMaxN];
+  float w[kMaxN];
+  float xi[kMaxN];
+};
+template <class T>
+struct TabOf;
+template <>
+struct TabOf<double> {
+  using type = Tables;
+};
+template <>
+struct TabOf<float> {
+  using type = TablesF;
+};
+
+template <class T>
+__device__ __forceinline__ T coeff_var_t(const T x[3]) {
+  return T(1) / (T(0.05) + T(2) * (x[0] * x[0] + x[1] * x[1] + x[2] * x[2]));  // R5
 }
 
 __device__ __forceinline__ double coeff_var(const double x[3], int dim) {
@@ -382,47 +405,83 @@ __global__ void __launch_bounds__(256) k_apply_general(const __grid_constant__ T
 //   7 R = G0 + G1 + gz, S_z^T         (-> U)
 //   8 S_y^T
 //   9 S_x^T in regs, scatter-add + identity rows
+// shared-memory layout of k_apply_cell3: work arrays [cpb][3 NV], then (curved cells) the
+// metric [6][chunk] with chunk = cpb NV rounded up to 16 bytes, starting 16-byte aligned
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr int cell3_ms_off();
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr int cell3_chunk();
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr size_t cell3_smem_bytes();
+
+// sizeof(T)-byte cp.async (zero-fill when !ok)
+template <class T>
+__device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(ok ? 4 : 0) : "memory");
+}
+
 // cells per block of k_apply_cell3: ~256 threads, ~128 with the staged metric
 // (6 NV doubles per cell of extra shared memory), shared memory <= 48 KB
-template <int K, int GEOM>
+template <int K, int GEOM, class T = double>
 __host__ __device__ constexpr int cell3_cpb() {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
-  constexpr int per_cell = 8 * (3 + (GEOM == 2 ? 6 : 0)) * NV;
+  constexpr int per_cell = (int)sizeof(T) * (3 + (GEOM == 2 ? 6 : 0)) * NV;
   int c = (GEOM == 2 ? 128 : 256) / NP;
   while (c > 1 && c * per_cell > 48 * 1024) --c;
   return c < 1 ? 1 : c;
 }
 
-template <int K, int GEOM>
-__global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tables t, const __grid_constant__ Geo g,
-                                                     const double *__restrict__ src, double *__restrict__ dst,
-                                                     const double *__restrict__ metric, int64_t cbeg,
-                                                     int64_t cend) {
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr int cell3_ms_off() {
+  constexpr int NV = (K + 1) * (K + 1) * (K + 1), E = 16 / (int)sizeof(T);
+  return (cell3_cpb<K, GEOM, T>() * 3 * NV + E - 1) / E * E;
+}
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr int cell3_chunk() {
+  constexpr int NV = (K + 1) * (K + 1) * (K + 1), E = 16 / (int)sizeof(T);
+  return (cell3_cpb<K, GEOM, T>() * NV + E - 1) / E * E;
+}
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr size_t cell3_smem_bytes() {
+  return sizeof(T) * (size_t)(cell3_ms_off<K, GEOM, T>() + (GEOM == 2 ? 6 * cell3_chunk<K, GEOM, T>() : 0));
+}
+
+template <int K, int GEOM, class T>
+__global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typename TabOf<T>::type t,
+                                                     const __grid_constant__ Geo g, const T *__restrict__ src,
+                                                     T *__restrict__ dst, const T *__restrict__ metric,
+                                                     int64_t cbeg, int64_t cend) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   constexpr int CS = 3 * NV;  // U, G0, G1 per cell (the z-gradient lives in registers)
-  constexpr int cpb = cell3_cpb<K, GEOM>();
-  extern __shared__ double sm[];
+  constexpr int cpb = cell3_cpb<K, GEOM, T>();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T *const sm = reinterpret_cast<T *>(smraw);
   const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
   const bool active = cl < cpb;
   const int64_t cell0 = cbeg + (int64_t)blockIdx.x * cpb, cell = cell0 + cl;  // cells [cbeg, cend)
   const bool valid = active && cell < cend;
-  double *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV;
-  double gz[N];  // z-pencil: Co_z Q (steps 3-5), then Co_z^T t_z (steps 5-7)
+  T *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV;
+  T gz[N];  // z-pencil: Co_z Q (steps 3-5), then Co_z^T t_z (steps 5-7)
   // curved cells: the block's metric [6][cpb][NV] is staged into shared memory by
   // cp.async at kernel start, so its HBM latency overlaps steps 1-4
-  double *Ms = sm + cpb * CS;
+  T *Ms = sm + cell3_ms_off<K, GEOM, T>();  // 16-byte aligned (bulk-copy destination)
   __shared__ alignas(8) unsigned long long mbar;
   bool bulk = false;
   if (GEOM == 2) {
-    constexpr int CH = cpb * NV;  // doubles per component chunk
+    constexpr int CH = cell3_chunk<K, GEOM, T>();  // padded component chunk (16-byte multiple)
     const int64_t cstride = ncells * NV;
     const int64_t rem = cend - cell0;
     const int ncb = rem < cpb ? (int)rem : cpb;
-    const unsigned bytes = (unsigned)ncb * NV * 8;
+    const unsigned bytes = (unsigned)(ncb * NV * sizeof(T));
     // one thread, six bulk copies (TMA engine) completing on an mbarrier; the
     // 8-byte cp.async loop covers chunks that are not 16-byte multiples
-    bulk = (bytes % 16 == 0) && ((cell0 * NV) % 2 == 0) && (cstride % 2 == 0) &&
+    bulk = (bytes % 16 == 0) && ((cell0 * NV * (int64_t)sizeof(T)) % 16 == 0) &&
+           ((cstride * (int64_t)sizeof(T)) % 16 == 0) &&
            ((reinterpret_cast<uintptr_t>(metric) & 15) == 0);
     if (bulk) {
       if (threadIdx.x == 0) {
@@ -443,13 +502,11 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
       const int avail = ncb * NV;
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
-        const double *gc = metric + c * cstride + cell0 * NV;
+        const T *gc = metric + c * cstride + cell0 * NV;
         for (int r = threadIdx.x; r < CH; r += blockDim.x) {
           const bool ok = r < avail;
           const unsigned sa = (unsigned)__cvta_generic_to_shared(Ms + c * CH + r);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(ok ? gc + r : metric),
-                       "r"(ok ? 8 : 0)
-                       : "memory");
+          cp_async_elem(Ms + c * CH + r, ok ? gc + r : metric, ok);
         }
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -464,7 +521,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
   }
   const int64_t Nx = g.N[0], plane = g.N[0] * g.N[1];
   const CellInfo ci = cell_info<3, K>(g, valid ? cell : ncells, ncells);
-  double a[N], b[N];
+  T a[N], b[N];
 
   // 1: gather the x-pencil (y = p % N, z = p / N), S along x
   if (active) {
@@ -522,34 +579,34 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ Tab
   if (active) {
     constexpr int NGC = 6;
     const int qx = p % N, qy = p / N;
-    const double *Gm = Ms + cl * NV + p;
-    double t2[N];
+    const T *Gm = Ms + cl * NV + p;
+    T t2[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double gr0 = G0[o2[i]], gr1 = G1[o2[i]], gr2 = gz[i];
-      double tt0, tt1, tt2;
+      const T gr0 = G0[o2[i]], gr1 = G1[o2[i]], gr2 = gz[i];
+      T tt0, tt1, tt2;
       if (GEOM == 2) {
-        double G[NGC];
+        T G[NGC];
 #pragma unroll
-        for (int c = 0; c < NGC; ++c) G[c] = Gm[c * cpb * NV + NP * i];
+        for (int c = 0; c < NGC; ++c) G[c] = Gm[c * cell3_chunk<K, GEOM, T>() + NP * i];
         tt0 = G[0] * gr0 + G[1] * gr1 + G[2] * gr2;
         tt1 = G[1] * gr0 + G[3] * gr1 + G[4] * gr2;
         tt2 = G[2] * gr0 + G[4] * gr1 + G[5] * gr2;
       } else {
-        double W = t.w[qx] * t.w[qy] * t.w[i];
+        T W = t.w[qx] * t.w[qy] * t.w[i];
         if (GEOM == 1) {
-          double x[3];
-          x[0] = g.lo[0] + g.h[0] * ((double)ci.cx + t.xi[qx]);
-          x[1] = g.lo[1] + g.h[1] * ((double)ci.cy + t.xi[qy]);
-          x[2] = g.lo[2] + g.h[2] * ((double)(ci.cz + g.cz0) + t.xi[i]);
-          W *= coeff_var(x, 3) * (g.h[0] * g.h[1] * g.h[2]);
-          tt0 = W / (g.h[0] * g.h[0]) * gr0;
-          tt1 = W / (g.h[1] * g.h[1]) * gr1;
-          tt2 = W / (g.h[2] * g.h[2]) * gr2;
+          T x[3];
+          x[0] = (T)g.lo[0] + (T)g.h[0] * ((T)ci.cx + t.xi[qx]);
+          x[1] = (T)g.lo[1] + (T)g.h[1] * ((T)ci.cy + t.xi[qy]);
+          x[2] = (T)g.lo[2] + (T)g.h[2] * ((T)(ci.cz + g.cz0) + t.xi[i]);
+          W *= coeff_var_t<T>(x) * (T)(g.h[0] * g.h[1] * g.h[2]);
+          tt0 = W / (T)(g.h[0] * g.h[0]) * gr0;
+          tt1 = W / (T)(g.h[1] * g.h[1]) * gr1;
+          tt2 = W / (T)(g.h[2] * g.h[2]) * gr2;
         } else {
-          tt0 = W * g.fcart[0] * gr0;
-          tt1 = W * g.fcart[1] * gr1;
-          tt2 = W * g.fcart[2] * gr2;
+          tt0 = W * (T)g.fcart[0] * gr0;
+          tt1 = W * (T)g.fcart[1] * gr1;
+          tt2 = W * (T)g.fcart[2] * gr2;
         }
       }
       G0[o2[i]] = tt0;
@@ -621,9 +678,13 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
     if (!v1) {
       constexpr int c3 = cell3_cpb<K, GEOM>();
       const int64_t b3 = (cend - cbeg + c3 - 1) / c3;
-      const size_t sm3 = (size_t)c3 * (3 + (GEOM == 2 ? 6 : 0)) * NV * sizeof(double);
-      k_apply_cell3<K, GEOM><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric, cbeg,
-                                                                                    cend);
+      const size_t sm3 = cell3_smem_bytes<K, GEOM, double>();
+      static bool attr = (cudaFuncSetAttribute(k_apply_cell3<K, GEOM, double>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3),
+                          true);
+      (void)attr;
+      k_apply_cell3<K, GEOM, double><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric,
+                                                                                            cbeg, cend);
       return cudaGetLastError();
     }
   }
@@ -651,6 +712,60 @@ static cudaError_t dispatch_k(const Geo &g, const Tables &t, const double *src, 
 static int geom_kind(const Geo &g) {
   if (g.geom == MF_GEOM_SINE) return 2;
   return g.coeff_kind == MF_COEFF_VARIABLE ? 1 : 0;
+}
+
+// FP32 instance of the 3D kernel over every cell (mixed-precision multigrid)
+template <int K, int GEOM>
+static cudaError_t launch_cell3_f32(const Geo &g, const TablesF &tf, const float *src, float *dst,
+                                    const float *metric, cudaStream_t s) {
+  constexpr int N = K + 1, NP = N * N;
+  constexpr int c3 = cell3_cpb<K, GEOM, float>();
+  const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
+  const int64_t b3 = (ncells + c3 - 1) / c3;
+  const size_t sm3 = cell3_smem_bytes<K, GEOM, float>();
+  static bool attr = (cudaFuncSetAttribute(k_apply_cell3<K, GEOM, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sm3),
+                      true);
+  (void)attr;
+  if (b3 == 0) return cudaSuccess;
+  k_apply_cell3<K, GEOM, float><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(tf, g, src, dst, metric, 0,
+                                                                                      ncells);
+  return cudaGetLastError();
+}
+
+template <int GEOM>
+static cudaError_t dispatch_f32(const Geo &g, const TablesF &tf, const float *src, float *dst, const float *metric,
+                                cudaStream_t s) {
+  switch (g.k) {
+    case 1: return launch_cell3_f32<1, GEOM>(g, tf, src, dst, metric, s);
+    case 2: return launch_cell3_f32<2, GEOM>(g, tf, src, dst, metric, s);
+    case 3: return launch_cell3_f32<3, GEOM>(g, tf, src, dst, metric, s);
+    case 4: return launch_cell3_f32<4, GEOM>(g, tf, src, dst, metric, s);
+    case 5: return launch_cell3_f32<5, GEOM>(g, tf, src, dst, metric, s);
+    case 6: return launch_cell3_f32<6, GEOM>(g, tf, src, dst, metric, s);
+    case 7: return launch_cell3_f32<7, GEOM>(g, tf, src, dst, metric, s);
+    case 8: return launch_cell3_f32<8, GEOM>(g, tf, src, dst, metric, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float *src, float *dst,
+                                     const float *metric, cudaStream_t s, int64_t *launches) {
+  if (g.dim != 3) return cudaErrorNotSupported;
+  TablesF tf;
+  for (int i = 0; i < kMaxN; ++i) {
+    for (int j = 0; j < kMaxN; ++j) {
+      tf.S[i][j] = (float)t.S[i][j];
+      tf.Co[i][j] = (float)t.Co[i][j];
+    }
+    tf.w[i] = (float)t.w[i];
+    tf.xi[i] = (float)t.xi[i];
+  }
+  ++*launches;
+  const int gk = geom_kind(g);
+  if (gk == 0) return dispatch_f32<0>(g, tf, src, dst, metric, s);
+  if (gk == 1) return dispatch_f32<1>(g, tf, src, dst, metric, s);
+  return dispatch_f32<2>(g, tf, src, dst, metric, s);
 }
 
 static cudaError_t general_range(const Geo &g, const Tables &t, const double *src, double *dst,

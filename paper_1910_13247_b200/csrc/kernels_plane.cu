@@ -42,19 +42,23 @@ struct PlaneShape {
   static constexpr int STG = N * SPL;           // u on planes 0..K of a layer
   static constexpr int FACE = N * N;
   static constexpr int NV = NCELL * N * FACE;   // P (or Q): faces of planes 0..K
-  static constexpr size_t SMEM = sizeof(double) * (STG + 2 * NV);
+  template <class T>
+  static constexpr size_t smem() { return sizeof(T) * (STG + 2 * NV); }
 };
 
-template <int K, int TX, int TY, bool ISO>
-__global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
-    k_apply_plane(const __grid_constant__ TileParams P, const double *__restrict__ src, double *__restrict__ dst) {
+template <int K, int TX, int TY, bool ISO, class T>
+__global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 : 3)
+    k_apply_plane(const __grid_constant__ TileParams P, const T *__restrict__ src, T *__restrict__ dst) {
   using S = PlaneShape<K, TX, TY>;
   constexpr int N = S::N, NXc = S::NXc, NCELL = S::NCELL, SPL = S::SPL, FACE = S::FACE;
   constexpr int h = (N + 1) / 2;
   constexpr int PSTRIDE = TX * FACE;       // face slot of (cx, cy, p) = cx + TX (p + N cy)
   constexpr int YSTRIDE = TX * N * FACE;   // cy -> cy + 1
-  extern __shared__ double sm[];
-  double *Us = sm, *Vp = sm + S::STG, *Vq = Vp + S::NV;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T *const sm = reinterpret_cast<T *>(smraw);
+  T *Us = sm, *Vp = sm + S::STG, *Vq = Vp + S::NV;
+  const EOMatT<T> &Mm = tp_M<T>(P), &Km = tp_K<T>(P);
+  const T ry = (T)P.ry, rz = (T)P.rz;
 
   const int ntile = P.ntx * P.nty, nitems = ntile * tile_pass_chunks(P);
   const int Nx = (int)P.Nx, Ny = (int)P.Ny;
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   // (constrained nodes are zero-filled: their addresses are valid vector entries,
   // only the byte count drops to 0)
   auto prefetch = [&](const Item &I, int cz, int l0) {
-    const double *sp0 = src + I.base0 + (int64_t)K * (cz - I.cz_begin) * plane;
+    const T *sp0 = src + I.base0 + (int64_t)K * (cz - I.cz_begin) * plane;
     const bool zlo = z_lo_c && cz == 0, zhi = z_hi_c && cz == P.ncz - 1;  // planes l = 0 / l = K
     const bool own_ok = ccx < I.nvx && ccy < I.nvy;
     const int y = K * ccy + jr;
@@ -118,8 +122,8 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
     int ex = 0, ey = 0;
     const bool has_e = edge_xy(I, ex, ey);
     const bool e_ok = has_e && !xy_cons(I, ex, ey);
-    const double *go = sp0 + y * Nx + K * ccx, *ge = sp0 + ey * Nx + ex;
-    double *so = Us + y * NXc + K * ccx, *se = Us + ey * NXc + ex;
+    const T *go = sp0 + y * Nx + K * ccx, *ge = sp0 + ey * Nx + ex;
+    T *so = Us + y * NXc + K * ccx, *se = Us + ey * NXc + ex;
 #pragma unroll
     for (int l = 0; l <= K; ++l) {
       if (l >= l0) {
@@ -128,10 +132,10 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             const bool ok = !zc && !ycons && !(i == 0 && xcons0);
-            cp_async8z(so + l * SPL + i, go + i, ok ? 8u : 0u);
+            cp_async_z<T>(so + l * SPL + i, go + i, ok ? 8u : 0u);
           }
         }
-        if (has_e) cp_async8z(se + l * SPL, ge, (e_ok && !zc) ? 8u : 0u);
+        if (has_e) cp_async_z<T>(se + l * SPL, ge, (e_ok && !zc) ? 8u : 0u);
       }
       go += plane;
       ge += plane;
@@ -141,42 +145,42 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
 
   // ---- face: P and Q on the face of cell (fcx, fcy) at plane p from u on that plane
   auto face = [&](int p) {
-    const double *Ul = Us + p * SPL + (K * fcy) * NXc + K * fcx;
-    double *Pf = Vp + (fcx + TX * (p + N * fcy)) * FACE, *Qf = Vq + (fcx + TX * (p + N * fcy)) * FACE;
-    double c[N][N], g[N][N];  // [j][i]: c = M_y u, g = Ky' u
+    const T *Ul = Us + p * SPL + (K * fcy) * NXc + K * fcx;
+    T *Pf = Vp + (fcx + TX * (p + N * fcy)) * FACE, *Qf = Vq + (fcx + TX * (p + N * fcy)) * FACE;
+    T c[N][N], g[N][N];  // [j][i]: c = M_y u, g = Ky' u
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      double uv[N], e[h], o[h], ve[h], vo[h], t[N];
+      T uv[N], e[h], o[h], ve[h], vo[h], t[N];
 #pragma unroll
       for (int j = 0; j < N; ++j) uv[j] = Ul[j * NXc + i];
       eo_split<N>(uv, e, o);
-      eo_first<N>(P.M, e, o, ve, vo);
+      eo_first<N>(Mm, e, o, ve, vo);
       eo_combine<N>(ve, vo, t);
 #pragma unroll
       for (int j = 0; j < N; ++j) c[j][i] = t[j];
       if (!ISO) {
 #pragma unroll
         for (int q = 0; q < h; ++q) {
-          e[q] *= P.ry;
-          o[q] *= P.ry;
+          e[q] *= ry;
+          o[q] *= ry;
         }
       }
-      eo_first<N>(P.K, e, o, ve, vo);
+      eo_first<N>(Km, e, o, ve, vo);
       eo_combine<N>(ve, vo, t);
 #pragma unroll
       for (int j = 0; j < N; ++j) g[j][i] = t[j];
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      double ec[h], oc[h], eg[h], og[h], ve[h], vo[h], t[N];
+      T ec[h], oc[h], eg[h], og[h], ve[h], vo[h], t[N];
       eo_split<N>(c[j], ec, oc);
       eo_split<N>(g[j], eg, og);
-      eo_first<N>(P.K, ec, oc, ve, vo);  // P = Kx' c + Mx g
-      eo_acc<N>(P.M, eg, og, ve, vo);
+      eo_first<N>(Km, ec, oc, ve, vo);  // P = Kx' c + Mx g
+      eo_acc<N>(Mm, eg, og, ve, vo);
       eo_combine<N>(ve, vo, t);
 #pragma unroll
       for (int i = 0; i < N; ++i) Pf[j * N + i] = t[i];
-      eo_first<N>(P.M, ec, oc, ve, vo);  // Q = Mx c
+      eo_first<N>(Mm, ec, oc, ve, vo);  // Q = Mx c
       eo_combine<N>(ve, vo, t);
 #pragma unroll
       for (int i = 0; i < N; ++i) Qf[j * N + i] = t[i];
@@ -186,20 +190,20 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   // ---- z-sweep of one column: v = Mz P + Kz' Q (even-odd), carries, stores
   // zm / am: the layer's planes l that are z-constrained / shared with the
   // neighbouring z-chunk (bit l, warp-uniform)
-  auto zcolumn = [&](const double *pb, const double *qb, double &vcar, bool first, bool last, bool cons, bool shared,
-                     double *out, uint32_t zm, uint32_t am) {
-    double e[h], o[h], ve[h], vo[h], v[N];
+  auto zcolumn = [&](const T *pb, const T *qb, T &vcar, bool first, bool last, bool cons, bool shared,
+                     T *out, uint32_t zm, uint32_t am) {
+    T e[h], o[h], ve[h], vo[h], v[N];
     eo_split<N>(pb, e, o);
-    eo_first<N>(P.M, e, o, ve, vo);
+    eo_first<N>(Mm, e, o, ve, vo);
     eo_split<N>(qb, e, o);
     if (!ISO) {
 #pragma unroll
       for (int q = 0; q < h; ++q) {
-        e[q] *= P.rz;
-        o[q] *= P.rz;
+        e[q] *= rz;
+        o[q] *= rz;
       }
     }
-    eo_acc<N>(P.K, e, o, ve, vo);
+    eo_acc<N>(Km, e, o, ve, vo);
     eo_combine<N>(ve, vo, v);
     if (!first) v[0] += vcar;
     vcar = v[K];
@@ -210,11 +214,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
       if (!((zm >> l) & 1u)) {
         // predicated red / st, no divergent branch (shared varies across lanes)
         const int at = (shared || ((am >> l) & 1u)) ? 1 : 0;
-        asm volatile(
-            "{\n .reg .pred pa;\n setp.ne.s32 pa, %2, 0;\n"
-            " @pa red.global.add.f64 [%0], %1;\n @!pa st.global.f64 [%0], %1;\n}\n" ::"l"(out),
-            "d"(v[l]), "r"(at)
-            : "memory");
+        red_or_st(out, v[l], at);
       }
       out += plane;
     }
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
   if (item >= nitems) return;
   Item G = item_of(item);
   prefetch(G, G.cz_begin, 0);
-  double pcar[K + 1], qcar[K + 1], vcar[K + 1];  // owned columns i = 0..K-1, [K] = edge column
+  T pcar[K + 1], qcar[K + 1], vcar[K + 1];  // owned columns i = 0..K-1, [K] = edge column
 
   while (true) {
     const int cz_begin = G.cz_begin, cz_end = G.cz_end, chunk = G.chunk;
@@ -287,11 +287,11 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
       }
       const uint32_t zm = ((z_lo_c && cz == 0) ? 1u : 0u) | ((z_hi_c && cz == P.ncz - 1) ? 1u << K : 0u);
       const uint32_t am = ((first && chunk > 0) ? 1u : 0u) | ((last && chunk < P.nch - 1) ? 1u << K : 0u);
-      double *outl = dst + base0 + (int64_t)K * (cz - cz_begin) * plane;
+      T *outl = dst + base0 + (int64_t)K * (cz - cz_begin) * plane;
       if (own_ok) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          double pb[N], qb[N];
+          T pb[N], qb[N];
 #pragma unroll
           for (int p = 0; p < N; ++p) {
             if (p == 0 && !first) {
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
               continue;
             }
             const int o = own0 + p * PSTRIDE + i;
-            double sp_ = Vp[o], sq_ = Vq[o];
+            T sp_ = Vp[o], sq_ = Vq[o];
             if (i == 0 && hasL) {  // left face, its local (K, jr)
               sp_ += Vp[o - FACE + K];
               sq_ += Vq[o - FACE + K];
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
         }
       }
       if (has_e) {
-        double pb[N], qb[N];
+        T pb[N], qb[N];
 #pragma unroll
         for (int p = 0; p < N; ++p) {
           if (p == 0 && !first) {
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
             qb[0] = qcar[K];
             continue;
           }
-          double sp_ = 0.0, sq_ = 0.0;
+          T sp_ = 0.0, sq_ = 0.0;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (eo[q] >= 0) {
@@ -354,16 +354,17 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, 2)
 
 // part 0: init + every chunk; part 1: init + the two boundary chunks of the z-split;
 // part 2: the interior chunks of the z-split (see TileParams::zsplit)
-template <int K, int TX, int TY, bool ISO>
-static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+template <int K, int TX, int TY, bool ISO, class T>
+static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T *dst, cudaStream_t s,
                                   int64_t *launches, int part) {
   using S = PlaneShape<K, TX, TY>;
   TileParams P;
   tile_params_common(g, t, TX, TY, &P);
   static int occ = 0, sms = 0;
   if (occ == 0) {
-    cudaFuncSetAttribute(k_apply_plane<K, TX, TY, ISO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_plane<K, TX, TY, ISO>, S::NT, S::SMEM);
+    cudaFuncSetAttribute(k_apply_plane<K, TX, TY, ISO, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::template smem<T>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_plane<K, TX, TY, ISO, T>, S::NT, S::template smem<T>());
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -383,18 +384,19 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const double *s
   if (items == 0) return cudaSuccess;
   ++*launches;
   const int blocks = std::min(items, slots);
-  k_apply_plane<K, TX, TY, ISO><<<blocks, S::NT, S::SMEM, s>>>(P, src, dst);
+  k_apply_plane<K, TX, TY, ISO, T><<<blocks, S::NT, S::template smem<T>(), s>>>(P, src, dst);
   return cudaGetLastError();
 }
 
 bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }
 
-cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
-                                    int64_t *launches, int part) {
+template <class T>
+static cudaError_t launch_cart_plane_any(const Geo &g, const Tables &t, const T *src, T *dst, cudaStream_t s,
+                                        int64_t *launches, int part) {
   const bool iso = g.fcart[0] == g.fcart[1] && g.fcart[0] == g.fcart[2];
-#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                                 \
-  return iso ? launch_plane_t<KK, TXX, TYY, true>(g, t, src, dst, s, launches, part)  \
-             : launch_plane_t<KK, TXX, TYY, false>(g, t, src, dst, s, launches, part)
+#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                                    \
+  return iso ? launch_plane_t<KK, TXX, TYY, true, T>(g, t, src, dst, s, launches, part)  \
+             : launch_plane_t<KK, TXX, TYY, false, T>(g, t, src, dst, s, launches, part)
   switch (g.k) {
     case 2: MF_PLANE_LAUNCH(2, 8, 8);
     case 3: MF_PLANE_LAUNCH(3, 8, 4);
@@ -402,6 +404,16 @@ cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double 
   }
 #undef MF_PLANE_LAUNCH
   return cudaErrorNotSupported;
+}
+
+cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+                                    int64_t *launches, int part) {
+  return launch_cart_plane_any<double>(g, t, src, dst, s, launches, part);
+}
+
+cudaError_t launch_apply_cart_plane_f32(const Geo &g, const Tables &t, const float *src, float *dst, cudaStream_t s,
+                                        int64_t *launches) {
+  return launch_cart_plane_any<float>(g, t, src, dst, s, launches, 0);
 }
 
 }  // namespace mf

@@ -212,4 +212,64 @@ cudaError_t launch_plane_add(double *dst, const double *recv, int64_t n, cudaStr
   return cudaGetLastError();
 }
 
+// ---- FP32 vector kernels of the mixed-precision multigrid (§8(f) f2) ----------
+__global__ void k_zero_f(float *x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = 0.f;
+}
+cudaError_t launch_zero_f(float *x, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_zero_f<<<grid_for(n), 256, 0, s>>>(x, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_d2f(const double *__restrict__ x, float *__restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)x[i];
+}
+__global__ void k_f2d(const float *__restrict__ x, double *__restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (double)x[i];
+}
+cudaError_t launch_d2f(const double *x, float *y, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_d2f<<<grid_for(n), 256, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_f2d(const float *x, double *y, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_f2d<<<grid_for(n), 256, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_cheb_init_f(const float *__restrict__ r, const float *__restrict__ dinv, float c0,
+                              float *__restrict__ x, float *__restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = r[i] * dinv[i] * c0;
+    x[i] = v;
+    d[i] = v;
+  }
+}
+cudaError_t launch_cheb_init_f(const float *r, const float *dinv, float c0, float *x, float *d, int64_t n,
+                               cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cheb_init_f<<<grid_for(n), 256, 0, s>>>(r, dinv, c0, x, d, n);
+  return cudaGetLastError();
+}
+
+__global__ void k_cheb_step_f(const float *__restrict__ r, const float *__restrict__ ax, const float *__restrict__ dinv,
+                              float c1, float c2, float *__restrict__ x, float *__restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float dn = c1 * d[i] + c2 * (dinv[i] * (r[i] - ax[i]));
+    d[i] = dn;
+    x[i] += dn;
+  }
+}
+cudaError_t launch_cheb_step_f(const float *r, const float *ax, const float *dinv, float c1, float c2, float *x,
+                               float *d, int64_t n, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cheb_step_f<<<grid_for(n), 256, 0, s>>>(r, ax, dinv, c1, c2, x, d, n);
+  return cudaGetLastError();
+}
+
 }  // namespace mf

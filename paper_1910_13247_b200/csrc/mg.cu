@@ -28,8 +28,9 @@ constexpr int kMaxK = 8;
 constexpr int64_t kMaxCoarse = 2048;
 
 // W[m][j] = l_j(t_m): coarse basis j at fine node m = 0..2k of one coarse cell
-struct Interp {
-  double W[2 * kMaxK + 1][kMaxK + 1];
+template <class T>
+struct InterpT {
+  T W[2 * kMaxK + 1][kMaxK + 1];
   int k;
 };
 
@@ -38,8 +39,9 @@ struct Dims {
 };
 
 // out (dims in, axis refined: n_out = 2 n_in - 1) = 1D interpolation along `axis`
-__global__ void k_interp_axis(const __grid_constant__ Interp I, int axis, Dims din, const double *__restrict__ in,
-                              double *__restrict__ out) {
+template <class T>
+__global__ void k_interp_axis(const __grid_constant__ InterpT<T> I, int axis, Dims din, const T *__restrict__ in,
+                              T *__restrict__ out) {
   const int k = I.k;
   Dims dout = din;
   dout.n[axis] = 2 * din.n[axis] - 1;
@@ -60,8 +62,8 @@ __global__ void k_interp_axis(const __grid_constant__ Interp I, int axis, Dims d
       m = 2 * k;
     }
     c[axis] = k * cc;
-    const double *ip = in + (c[2] * din.n[1] + c[1]) * din.n[0] + c[0];
-    double s = 0.0;
+    const T *ip = in + (c[2] * din.n[1] + c[1]) * din.n[0] + c[0];
+    T s = 0;
     for (int j = 0; j <= k; ++j) s = fma(I.W[m][j], ip[j * sin], s);
     out[o] = s;
   }
@@ -71,8 +73,9 @@ __global__ void k_interp_axis(const __grid_constant__ Interp I, int axis, Dims d
 // transpose of k_interp_axis: coarse node c = k cc + j gathers the fine nodes of the
 // coarse cells containing it; a fine node on a coarse vertex belongs to the cell on its
 // right (the last one to the last cell), exactly as in k_interp_axis
-__global__ void k_restrict_axis(const __grid_constant__ Interp I, int axis, Dims dout, const double *__restrict__ in,
-                                double *__restrict__ out) {
+template <class T>
+__global__ void k_restrict_axis(const __grid_constant__ InterpT<T> I, int axis, Dims dout, const T *__restrict__ in,
+                                T *__restrict__ out) {
   const int k = I.k;
   Dims din = dout;
   din.n[axis] = 2 * dout.n[axis] - 1;
@@ -88,8 +91,8 @@ __global__ void k_restrict_axis(const __grid_constant__ Interp I, int axis, Dims
     const int64_t cn = c[axis], cc = cn / k;
     const int j = (int)(cn - k * cc);
     c[axis] = 0;
-    const double *ip = in + (c[2] * din.n[1] + c[1]) * din.n[0] + c[0];
-    double s = 0.0;
+    const T *ip = in + (c[2] * din.n[1] + c[1]) * din.n[0] + c[0];
+    T s = 0;
     if (j != 0) {
       for (int m = 0; m <= 2 * k; ++m) s = fma(I.W[m][j], ip[(2 * k * cc + m) * sin], s);
     } else {
@@ -103,22 +106,28 @@ __global__ void k_restrict_axis(const __grid_constant__ Interp I, int axis, Dims
   }
 }
 
-__global__ void k_zero_constrained(double *__restrict__ x, Dims d, uint32_t dir) {
+template <class T>
+__global__ void k_zero_constrained(T *__restrict__ x, Dims d, uint32_t dir) {
   const int64_t total = d.n[0] * d.n[1] * d.n[2];
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t gx = o % d.n[0], r = o / d.n[0], gy = r % d.n[1], gz = r / d.n[1];
     const bool cons = ((dir & 1u) && gx == 0) || ((dir & 2u) && gx == d.n[0] - 1) || ((dir & 4u) && gy == 0) ||
                       ((dir & 8u) && gy == d.n[1] - 1) || ((dir & 16u) && gz == 0) ||
                       ((dir & 32u) && gz == d.n[2] - 1);
-    if (cons) x[o] = 0.0;
+    if (cons) x[o] = T(0);
   }
 }
 
 // y = a x + b y (element-wise combination used by the V-cycle)
-__global__ void k_axpby2(double a, const double *__restrict__ x, double b, const double *__restrict__ y,
-                         double *__restrict__ out, int64_t n) {
+template <class T>
+__global__ void k_axpby2(T a, const T *__restrict__ x, T b, const T *__restrict__ y, T *__restrict__ out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = a * x[i] + b * y[i];
+}
+
+__global__ void k_d2f_mg(const double *__restrict__ x, float *__restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)x[i];
 }
 
 __global__ void k_unit(double *x, int64_t n, int64_t j) {
@@ -139,12 +148,12 @@ __global__ void k_gj_step(const double *__restrict__ M, double *__restrict__ Mo,
 }
 
 // y = A x, A row-major n x n with leading dimension lda; one warp per row
-__global__ void k_gemv(const double *__restrict__ A, int64_t lda, const double *__restrict__ x, double *__restrict__ y,
-                       int64_t n) {
+template <class T>
+__global__ void k_gemv(const T *__restrict__ A, int64_t lda, const T *__restrict__ x, T *__restrict__ y, int64_t n) {
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
-  double s = 0.0;
+  T s = 0;
   for (int64_t j = lane; j < n; j += 32) s = fma(A[row * lda + j], x[j], s);
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) y[row] = s;
@@ -165,23 +174,58 @@ double lagrange(const double *x, int k, int j, double t) {
 
 }  // namespace
 
+// the V-cycle's vectors in one precision
+template <class T>
+struct MGBufs {
+  // per level: b, x (levels < L-1, all levels for FP32), r, t, z (levels >= 1)
+  std::vector<T *> b, x, r, t, z;
+  T *tmp1 = nullptr, *tmp2 = nullptr;  // transfer intermediates (<= finest size)
+  T *ainv = nullptr;                   // dense inverse of level 0, n0 x n0 row-major
+  InterpT<T> I;
+  void free_all() {
+    for (auto *v : {&b, &x, &r, &t, &z})
+      for (T *p : *v) cudaFree(p);
+    cudaFree(tmp1);
+    cudaFree(tmp2);
+    cudaFree(ainv);
+  }
+};
+
 struct mf_mg {
   int L = 0, k = 0;
   uint32_t dirichlet = 0;
+  int precision = 0;  // 0 FP64 V-cycle, 1 FP32 V-cycle
   std::vector<mf_op *> ops;
   std::vector<Dims> dims;
   std::vector<int64_t> n;
   std::vector<double> lam;
-  // per level: b, x (levels < L-1), r, t, z (levels >= 1)
-  std::vector<double *> b, x, r, t, z;
-  double *tmp1 = nullptr, *tmp2 = nullptr;  // transfer intermediates (<= finest size)
-  double *ainv = nullptr;                   // dense inverse of level 0, n0 x n0 row-major
-  Interp I;
+  MGBufs<double> d;
+  MGBufs<float> f;
   int degree = 6;
   double range = 20.0;
   cudaStream_t stream = 0;
   int64_t launches = 0;
 };
+
+template <class T>
+static MGBufs<T> &bufs(mf_mg *mg);
+template <>
+MGBufs<double> &bufs<double>(mf_mg *mg) {
+  return mg->d;
+}
+template <>
+MGBufs<float> &bufs<float>(mf_mg *mg) {
+  return mg->f;
+}
+// the level operator and smoother in precision T
+static mf_status level_apply(mf_op *op, const double *x, double *y, int64_t n) { return mf_apply(op, x, n, y, n); }
+static mf_status level_apply(mf_op *op, const float *x, float *y, int64_t) { return apply_f32(op, x, y); }
+static mf_status level_cheb(mf_mg *mg, int l, const double *r, double *x) {
+  return mf_chebyshev(mg->ops[l], r, x, mg->n[l], mg->lam[l], mg->degree, mg->range);
+}
+static mf_status level_cheb(mf_mg *mg, int l, const float *r, float *x) {
+  return cheb_f32(mg->ops[l], r, x, mg->lam[l], mg->degree, mg->range);
+}
 
 #define MG_CUDA(call)                                                                   \
   do {                                                                                  \
@@ -196,24 +240,27 @@ struct mf_mg {
     if (s_ != MF_OK) return s_;   \
   } while (0)
 
-static mf_status zero_constrained(mf_mg *mg, int l, double *v) {
+template <class T>
+static mf_status zero_constrained(mf_mg *mg, int l, T *v) {
   if (!mg->dirichlet) return MF_OK;
   ++mg->launches;
-  k_zero_constrained<<<grid_for(mg->n[l]), 256, 0, mg->stream>>>(v, mg->dims[l], mg->dirichlet);
+  k_zero_constrained<T><<<grid_for(mg->n[l]), 256, 0, mg->stream>>>(v, mg->dims[l], mg->dirichlet);
   MG_CUDA(cudaGetLastError());
   return MF_OK;
 }
 
 // fine(l) = P coarse(l-1), then the fine constrained DoFs zeroed
-static mf_status prolongate(mf_mg *mg, int l, const double *coarse, double *fine) {
+template <class T>
+static mf_status prolongate(mf_mg *mg, int l, const T *coarse, T *fine) {
+  MGBufs<T> &B = bufs<T>(mg);
   Dims d = mg->dims[l - 1];
-  const double *in = coarse;
-  double *bufs[3] = {mg->tmp1, mg->tmp2, fine};
+  const T *in = coarse;
+  T *bufs[3] = {B.tmp1, B.tmp2, fine};
   for (int axis = 0; axis < 3; ++axis) {
     Dims dn = d;
     dn.n[axis] = 2 * d.n[axis] - 1;
     ++mg->launches;
-    k_interp_axis<<<grid_for(dn.n[0] * dn.n[1] * dn.n[2]), 256, 0, mg->stream>>>(mg->I, axis, d, in, bufs[axis]);
+    k_interp_axis<T><<<grid_for(dn.n[0] * dn.n[1] * dn.n[2]), 256, 0, mg->stream>>>(B.I, axis, d, in, bufs[axis]);
     MG_CUDA(cudaGetLastError());
     in = bufs[axis];
     d = dn;
@@ -223,16 +270,18 @@ static mf_status prolongate(mf_mg *mg, int l, const double *coarse, double *fine
 
 // coarse(l-1) = P^T fine(l) (fine constrained entries must already be 0), then the
 // coarse constrained DoFs zeroed
-static mf_status restrict_(mf_mg *mg, int l, const double *fine, double *coarse) {
+template <class T>
+static mf_status restrict_(mf_mg *mg, int l, const T *fine, T *coarse) {
+  MGBufs<T> &B = bufs<T>(mg);
   Dims d = mg->dims[l];
-  const double *in = fine;
-  double *bufs[3] = {mg->tmp1, mg->tmp2, coarse};
+  const T *in = fine;
+  T *bufs[3] = {B.tmp1, B.tmp2, coarse};
   for (int s = 0; s < 3; ++s) {
     const int axis = 2 - s;
     Dims dn = d;
     dn.n[axis] = (d.n[axis] + 1) / 2;
     ++mg->launches;
-    k_restrict_axis<<<grid_for(dn.n[0] * dn.n[1] * dn.n[2]), 256, 0, mg->stream>>>(mg->I, axis, dn, in, bufs[s]);
+    k_restrict_axis<T><<<grid_for(dn.n[0] * dn.n[1] * dn.n[2]), 256, 0, mg->stream>>>(B.I, axis, dn, in, bufs[s]);
     MG_CUDA(cudaGetLastError());
     in = bufs[s];
     d = dn;
@@ -240,45 +289,56 @@ static mf_status restrict_(mf_mg *mg, int l, const double *fine, double *coarse)
   return zero_constrained(mg, l - 1, coarse);
 }
 
-static mf_status axpby2(mf_mg *mg, double a, const double *x, double b, const double *y, double *out, int64_t n) {
+template <class T>
+static mf_status axpby2(mf_mg *mg, T a, const T *x, T b, const T *y, T *out, int64_t n) {
   ++mg->launches;
-  k_axpby2<<<grid_for(n), 256, 0, mg->stream>>>(a, x, b, y, out, n);
+  k_axpby2<T><<<grid_for(n), 256, 0, mg->stream>>>(a, x, b, y, out, n);
   MG_CUDA(cudaGetLastError());
   return MF_OK;
 }
 
-// x_l = V_l(b_l)
-static mf_status vcycle(mf_mg *mg, int l, const double *b, double *x) {
+// x_l = V_l(b_l), in precision T
+template <class T>
+static mf_status vcycle(mf_mg *mg, int l, const T *b, T *x) {
+  MGBufs<T> &B = bufs<T>(mg);
   const int64_t n = mg->n[l];
   if (l == 0) {
     ++mg->launches;
-    k_gemv<<<(unsigned)((n * 32 + 255) / 256), 256, 0, mg->stream>>>(mg->ainv, n, b, x, n);
+    k_gemv<T><<<(unsigned)((n * 32 + 255) / 256), 256, 0, mg->stream>>>(B.ainv, n, b, x, n);
     MG_CUDA(cudaGetLastError());
     return MF_OK;
   }
   mf_op *op = mg->ops[l];
-  double *r = mg->r[l], *t = mg->t[l], *z = mg->z[l];
-  MG_TRY(mf_chebyshev(op, b, x, n, mg->lam[l], mg->degree, mg->range));  // pre-smoothing from 0
-  MG_TRY(mf_apply(op, x, n, t, n));
-  MG_TRY(axpby2(mg, 1.0, b, -1.0, t, r, n));  // r = b - A x
+  T *r = B.r[l], *t = B.t[l], *z = B.z[l];
+  MG_TRY(level_cheb(mg, l, b, x));  // pre-smoothing from 0
+  MG_TRY(level_apply(op, x, t, n));
+  MG_TRY(axpby2<T>(mg, T(1), b, T(-1), t, r, n));  // r = b - A x
   MG_TRY(zero_constrained(mg, l, r));
-  MG_TRY(restrict_(mg, l, r, mg->b[l - 1]));
-  MG_TRY(vcycle(mg, l - 1, mg->b[l - 1], mg->x[l - 1]));
-  MG_TRY(prolongate(mg, l, mg->x[l - 1], t));
-  MG_TRY(axpby2(mg, 1.0, x, 1.0, t, x, n));  // x += P x_c
-  MG_TRY(mf_apply(op, x, n, t, n));
-  MG_TRY(axpby2(mg, 1.0, b, -1.0, t, r, n));
-  MG_TRY(mf_chebyshev(op, r, z, n, mg->lam[l], mg->degree, mg->range));  // post-smoothing
-  return axpby2(mg, 1.0, x, 1.0, z, x, n);
+  MG_TRY(restrict_(mg, l, (const T *)r, B.b[l - 1]));
+  MG_TRY(vcycle(mg, l - 1, (const T *)B.b[l - 1], B.x[l - 1]));
+  MG_TRY(prolongate(mg, l, (const T *)B.x[l - 1], t));
+  MG_TRY(axpby2<T>(mg, T(1), x, T(1), t, x, n));  // x += P x_c
+  MG_TRY(level_apply(op, x, t, n));
+  MG_TRY(axpby2<T>(mg, T(1), b, T(-1), t, r, n));
+  MG_TRY(level_cheb(mg, l, (const T *)r, z));  // post-smoothing
+  return axpby2<T>(mg, T(1), x, T(1), z, x, n);
+}
+
+// z = V(r) on the finest level in the hierarchy's precision (FP64 in / out)
+static mf_status vcycle_top(mf_mg *mg, const double *r, double *z) {
+  const int top = mg->L - 1;
+  if (mg->precision == 0) return vcycle<double>(mg, top, r, z);
+  const int64_t n = mg->n[top];
+  MG_CUDA(launch_d2f(r, mg->f.b[top], n, mg->stream, &mg->launches));
+  MG_TRY(vcycle<float>(mg, top, mg->f.b[top], mg->f.x[top]));
+  MG_CUDA(launch_f2d(mg->f.x[top], z, n, mg->stream, &mg->launches));
+  return MF_OK;
 }
 
 extern "C" void mf_mg_destroy(mf_mg *mg) {
   if (!mg) return;
-  for (auto *v : {&mg->b, &mg->x, &mg->r, &mg->t, &mg->z})
-    for (double *p : *v) cudaFree(p);
-  cudaFree(mg->tmp1);
-  cudaFree(mg->tmp2);
-  cudaFree(mg->ainv);
+  mg->d.free_all();
+  mg->f.free_all();
   for (mf_op *op : mg->ops) mf_destroy(op);
   delete mg;
 }
@@ -292,7 +352,7 @@ extern "C" mf_status mf_mg_create(const mf_mesh *finest, int32_t degree, const m
   if ((finest->dirichlet_faces & 63u) == 0)
     return mf_set_error(MF_ERR_SINGULAR, "multigrid: pure Neumann operator is singular (no coarse inverse)");
   if (prm->smooth_degree < 1 || !(prm->smooth_range > 1.0) || !(prm->smooth_safety > 0.0) || prm->eig_cg_steps < 1 ||
-      prm->n_levels < 0)
+      prm->n_levels < 0 || prm->precision < 0 || prm->precision > 1)
     return mf_set_error(MF_ERR_ARGUMENT, "multigrid: bad smoother parameters");
   int64_t nc[3] = {finest->n_cells[0], finest->n_cells[1], finest->n_cells[2]};
   int L = prm->n_levels;
@@ -337,30 +397,44 @@ extern "C" mf_status mf_mg_create(const mf_mesh *finest, int32_t degree, const m
   // 1D interpolation weights from the library's own GLL nodes
   Tables tab;
   build_tables(degree, &tab);
-  std::memset(&mg->I, 0, sizeof(mg->I));
-  mg->I.k = degree;
+  std::memset(&mg->d.I, 0, sizeof(mg->d.I));
+  std::memset(&mg->f.I, 0, sizeof(mg->f.I));
+  mg->d.I.k = mg->f.I.k = degree;
   for (int m = 0; m <= 2 * degree; ++m) {
     const int child = m < degree ? 0 : (m < 2 * degree ? 1 : 2);
     const double tm = child == 2 ? 1.0 : 0.5 * (child + tab.gll[m - child * degree]);
-    for (int j = 0; j <= degree; ++j) mg->I.W[m][j] = lagrange(tab.gll, degree, j, tm);
+    for (int j = 0; j <= degree; ++j) {
+      mg->d.I.W[m][j] = lagrange(tab.gll, degree, j, tm);
+      mg->f.I.W[m][j] = (float)mg->d.I.W[m][j];
+    }
   }
   // vectors
   const size_t bytes_f = mg->n[L - 1] * sizeof(double);
-  mg->b.assign(L, nullptr);
-  mg->x.assign(L, nullptr);
-  mg->r.assign(L, nullptr);
-  mg->t.assign(L, nullptr);
-  mg->z.assign(L, nullptr);
-  for (int l = 0; l < L; ++l) {
-    const size_t bytes = mg->n[l] * sizeof(double);
-    if (l < L - 1 && (cudaMalloc(&mg->b[l], bytes) != cudaSuccess || cudaMalloc(&mg->x[l], bytes) != cudaSuccess))
-      return cleanup(mf_set_error(MF_ERR_OUT_OF_MEMORY, "multigrid vectors"));
-    if (l >= 1 && (cudaMalloc(&mg->r[l], bytes) != cudaSuccess || cudaMalloc(&mg->t[l], bytes) != cudaSuccess ||
-                   cudaMalloc(&mg->z[l], bytes) != cudaSuccess))
-      return cleanup(mf_set_error(MF_ERR_OUT_OF_MEMORY, "multigrid vectors"));
-  }
-  if (cudaMalloc(&mg->tmp1, bytes_f) != cudaSuccess || cudaMalloc(&mg->tmp2, bytes_f) != cudaSuccess)
-    return cleanup(mf_set_error(MF_ERR_OUT_OF_MEMORY, "multigrid transfer buffers"));
+  // FP64 buffers (always: the public transfer calls and the FP64 V-cycle), FP32 ones for
+  // the mixed-precision V-cycle
+  auto alloc = [&](auto &B, size_t es, bool all_bx) -> bool {
+    B.b.assign(L, nullptr);
+    B.x.assign(L, nullptr);
+    B.r.assign(L, nullptr);
+    B.t.assign(L, nullptr);
+    B.z.assign(L, nullptr);
+    for (int l = 0; l < L; ++l) {
+      const size_t bytes = mg->n[l] * es;
+      if ((l < L - 1 || all_bx) && (cudaMalloc((void **)&B.b[l], bytes) != cudaSuccess ||
+                                    cudaMalloc((void **)&B.x[l], bytes) != cudaSuccess))
+        return false;
+      if (l >= 1 && (cudaMalloc((void **)&B.r[l], bytes) != cudaSuccess ||
+                     cudaMalloc((void **)&B.t[l], bytes) != cudaSuccess ||
+                     cudaMalloc((void **)&B.z[l], bytes) != cudaSuccess))
+        return false;
+    }
+    return cudaMalloc((void **)&B.tmp1, mg->n[L - 1] * es) == cudaSuccess &&
+           cudaMalloc((void **)&B.tmp2, mg->n[L - 1] * es) == cudaSuccess;
+  };
+  (void)bytes_f;
+  mg->precision = prm->precision;
+  if (!alloc(mg->d, sizeof(double), false) || (mg->precision == 1 && !alloc(mg->f, sizeof(float), true)))
+    return cleanup(mf_set_error(MF_ERR_OUT_OF_MEMORY, "multigrid vectors"));
   // smoother intervals
   mg->lam.assign(L, 0.0);
   for (int l = 1; l < L; ++l) {
@@ -376,7 +450,8 @@ extern "C" mf_status mf_mg_create(const mf_mesh *finest, int32_t degree, const m
   const size_t abytes = (size_t)m0 * 2 * m0 * sizeof(double);
   if (cudaMalloc(&aug, abytes) != cudaSuccess || cudaMalloc(&aug2, abytes) != cudaSuccess ||
       cudaMalloc(&e, m0 * sizeof(double)) != cudaSuccess || cudaMalloc(&col, m0 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&mg->ainv, (size_t)m0 * m0 * sizeof(double)) != cudaSuccess) {
+      cudaMalloc(&mg->d.ainv, (size_t)m0 * m0 * sizeof(double)) != cudaSuccess ||
+      (mg->precision == 1 && cudaMalloc(&mg->f.ainv, (size_t)m0 * m0 * sizeof(float)) != cudaSuccess)) {
     cudaFree(aug);
     cudaFree(aug2);
     cudaFree(e);
@@ -399,8 +474,12 @@ extern "C" mf_status mf_mg_create(const mf_mesh *finest, int32_t degree, const m
     ce = cudaGetLastError();
   }
   if (st == MF_OK && ce == cudaSuccess)
-    ce = cudaMemcpy2DAsync(mg->ainv, m0 * sizeof(double), aug + m0, 2 * m0 * sizeof(double), m0 * sizeof(double), m0,
+    ce = cudaMemcpy2DAsync(mg->d.ainv, m0 * sizeof(double), aug + m0, 2 * m0 * sizeof(double), m0 * sizeof(double), m0,
                            cudaMemcpyDeviceToDevice, mg->stream);
+  if (ce == cudaSuccess && mg->precision == 1) {
+    k_d2f_mg<<<grid_for(m0 * m0), 256, 0, mg->stream>>>(mg->d.ainv, mg->f.ainv, m0 * m0);
+    ce = cudaGetLastError();
+  }
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(mg->stream);
   cudaFree(aug);
   cudaFree(aug2);
@@ -440,7 +519,7 @@ extern "C" mf_status mf_mg_prolongate(mf_mg *mg, int32_t level, const double *co
   if (!mg || !coarse || !fine || level < 1 || level >= mg->L) return mf_set_error(MF_ERR_ARGUMENT, "bad level");
   // the masked prolongation D_f P D_c: zero the coarse constrained entries first (the
   // V-cycle's coarse corrections are zero there already)
-  double *xc = mg->x[level - 1];
+  double *xc = mg->d.x[level - 1];
   MG_CUDA(cudaMemcpyAsync(xc, coarse, mg->n[level - 1] * sizeof(double), cudaMemcpyDeviceToDevice, mg->stream));
   MG_TRY(zero_constrained(mg, level - 1, xc));
   return prolongate(mg, level, xc, fine);
@@ -449,16 +528,17 @@ extern "C" mf_status mf_mg_prolongate(mf_mg *mg, int32_t level, const double *co
 extern "C" mf_status mf_mg_restrict(mf_mg *mg, int32_t level, const double *fine, double *coarse) {
   if (!mg || !coarse || !fine || level < 1 || level >= mg->L) return mf_set_error(MF_ERR_ARGUMENT, "bad level");
   // the transpose of the masked prolongation: zero the fine constrained entries first
-  MG_CUDA(cudaMemcpyAsync(mg->r[level], fine, mg->n[level] * sizeof(double), cudaMemcpyDeviceToDevice, mg->stream));
-  MG_TRY(zero_constrained(mg, level, mg->r[level]));
-  return restrict_(mg, level, mg->r[level], coarse);
+  MG_CUDA(cudaMemcpyAsync(mg->d.r[level], fine, mg->n[level] * sizeof(double), cudaMemcpyDeviceToDevice,
+                          mg->stream));
+  MG_TRY(zero_constrained(mg, level, mg->d.r[level]));
+  return restrict_(mg, level, (const double *)mg->d.r[level], coarse);
 }
 
 extern "C" mf_status mf_mg_vcycle(mf_mg *mg, const double *b, double *x, int64_t n) {
   if (!mg || !b || !x) return mf_set_error(MF_ERR_ARGUMENT, "null argument");
   if (n != mg->n[mg->L - 1]) return mf_set_error(MF_ERR_LENGTH, "vector length != finest n_local");
   if (b == x) return mf_set_error(MF_ERR_ARGUMENT, "b and x must be distinct");
-  return vcycle(mg, mg->L - 1, b, x);
+  return vcycle_top(mg, b, x);
 }
 
 extern "C" mf_status mf_mg_cg_solve(mf_mg *mg, const double *b, double *x, int64_t n, double rel_tol,
@@ -467,7 +547,7 @@ extern "C" mf_status mf_mg_cg_solve(mf_mg *mg, const double *b, double *x, int64
   if (n != mg->n[mg->L - 1]) return mf_set_error(MF_ERR_LENGTH, "vector length != finest n_local");
   if (!(rel_tol > 0.0) || max_iter < 1) return mf_set_error(MF_ERR_ARGUMENT, "bad CG parameters");
   result->lambda_max = mg->lam[mg->L - 1];
-  auto precond = [&](const double *r, double *z) -> mf_status { return vcycle(mg, mg->L - 1, r, z); };
+  auto precond = [&](const double *r, double *z) -> mf_status { return vcycle_top(mg, r, z); };
   return cg_core(mg->ops[mg->L - 1], b, x, rel_tol, max_iter, precond, result, history, history_cap);
 }
 

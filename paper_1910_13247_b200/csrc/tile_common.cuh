@@ -14,10 +14,12 @@ namespace mf {
 
 constexpr int kMaxH = 5;  // (kMaxN + 1) / 2
 
-struct EOMat {
-  double E[kMaxH][kMaxH];  // even part (rows i < h, cols j < h; col m = middle for odd n)
-  double O[kMaxH][kMaxH];  // odd part (rows/cols < n/2)
+template <class T>
+struct EOMatT {
+  T E[kMaxH][kMaxH];  // even part (rows i < h, cols j < h; col m = middle for odd n)
+  T O[kMaxH][kMaxH];  // odd part (rows/cols < n/2)
 };
+using EOMat = EOMatT<double>;
 
 // sm_100 DFMA takes no constant-bank operand: coefficients live in the 64-entry
 // uniform register file, so only two EO matrices are kept -- M and K = f_x K_ref --
@@ -26,6 +28,8 @@ struct EOMat {
 struct TileParams {
   EOMat M, K;
   double ry, rz;
+  EOMatT<float> Mf, Kf;  // the same in FP32 (mixed-precision multigrid, §8(f) f2)
+  float ryf, rzf;
   int64_t Nx, Ny, Nz;  // local node counts
   int ncx, ncy, ncz;   // local cell counts
   int ntx, nty, nch, LZ;
@@ -44,8 +48,22 @@ struct EO {
   static constexpr int m = N / 2, h = (N + 1) / 2;
 };
 
-template <int N>
-__device__ __forceinline__ void eo_split(const double *u, double *e, double *o) {
+// the coefficient set of scalar type T
+template <class T>
+__device__ __forceinline__ const EOMatT<T> &tp_M(const TileParams &P);
+template <>
+__device__ __forceinline__ const EOMatT<double> &tp_M<double>(const TileParams &P) { return P.M; }
+template <>
+__device__ __forceinline__ const EOMatT<float> &tp_M<float>(const TileParams &P) { return P.Mf; }
+template <class T>
+__device__ __forceinline__ const EOMatT<T> &tp_K(const TileParams &P);
+template <>
+__device__ __forceinline__ const EOMatT<double> &tp_K<double>(const TileParams &P) { return P.K; }
+template <>
+__device__ __forceinline__ const EOMatT<float> &tp_K<float>(const TileParams &P) { return P.Kf; }
+
+template <int N, class T>
+__device__ __forceinline__ void eo_split(const T *u, T *e, T *o) {
   constexpr int m = N / 2;
 #pragma unroll
   for (int j = 0; j < m; ++j) {
@@ -56,8 +74,8 @@ __device__ __forceinline__ void eo_split(const double *u, double *e, double *o) 
 }
 
 // ve += E e, vo += O o
-template <int N>
-__device__ __forceinline__ void eo_acc(const EOMat &A, const double *e, const double *o, double *ve, double *vo) {
+template <int N, class T>
+__device__ __forceinline__ void eo_acc(const EOMatT<T> &A, const T *e, const T *o, T *ve, T *vo) {
   constexpr int m = N / 2, h = (N + 1) / 2;
 #pragma unroll
   for (int i = 0; i < h; ++i)
@@ -69,8 +87,8 @@ __device__ __forceinline__ void eo_acc(const EOMat &A, const double *e, const do
     for (int j = 0; j < m; ++j) vo[i] = fma(A.O[i][j], o[j], vo[i]);
 }
 
-template <int N>
-__device__ __forceinline__ void eo_first(const EOMat &A, const double *e, const double *o, double *ve, double *vo) {
+template <int N, class T>
+__device__ __forceinline__ void eo_first(const EOMatT<T> &A, const T *e, const T *o, T *ve, T *vo) {
   constexpr int m = N / 2, h = (N + 1) / 2;
 #pragma unroll
   for (int i = 0; i < h; ++i) {
@@ -86,8 +104,8 @@ __device__ __forceinline__ void eo_first(const EOMat &A, const double *e, const 
   }
 }
 
-template <int N>
-__device__ __forceinline__ void eo_combine(const double *ve, const double *vo, double *v) {
+template <int N, class T>
+__device__ __forceinline__ void eo_combine(const T *ve, const T *vo, T *v) {
   constexpr int m = N / 2;
 #pragma unroll
   for (int i = 0; i < m; ++i) {
@@ -109,9 +127,10 @@ struct PlaneSet {
   int nfam;
 };
 
+template <class T>
 static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant__ TileParams P,
                                                            const __grid_constant__ PlaneSet ps,
-                                                           const double *__restrict__ src, double *__restrict__ dst) {
+                                                           const T *__restrict__ src, T *__restrict__ dst) {
   // one warp per line of a plane (x-plane: line gz, nodes gy; y-plane: line gz,
   // nodes gx; z-plane: line gy, nodes gx), warps grid-stride over all lines
   const int Nx = (int)P.Nx, Ny = (int)P.Ny, Nz = (int)P.Nz;
@@ -126,7 +145,7 @@ static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant_
     const int nlines = axis == 2 ? Ny : Nz, nnodes = axis == 0 ? Ny : Nx;
     const int pl = (int)(l / nlines), line = (int)(l - (int64_t)pl * nlines);
     const int c = (int)(ps.c0[f] + ps.stride[f] * pl);
-    if (axis == 0 && c >= 4 && c + 4 < Nx && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
+    if (sizeof(T) == 8 && axis == 0 && c >= 4 && c + 4 < Nx && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
       // strided x-plane nodes: write the whole aligned 32-byte sector around each
       // node instead of 8 bytes of it (no partial-sector writes).  The sector
       // stays inside the row, off the x faces (4 <= c < Nx - 4); its other nodes are
@@ -139,19 +158,19 @@ static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant_
         const bool ycons = ((d & 4u) && a == 0) || ((d & 8u) && a == Ny - 1) || ((d & 16u) && line == 0) ||
                            ((d & 32u) && line == Nz - 1);
         const bool ident = ycons && !(P.skip_top_identity && line == Nz - 1);
-        double v[4];
+        T v[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = ident ? __ldg(src + g0 + q) : 0.0;
+        for (int q = 0; q < 4; ++q) v[q] = ident ? __ldg(src + g0 + q) : T(0);
         double2 *p = reinterpret_cast<double2 *>(dst + g0);
-        p[0] = make_double2(v[0], v[1]);
-        p[1] = make_double2(v[2], v[3]);
+        p[0] = make_double2((double)v[0], (double)v[1]);
+        p[1] = make_double2((double)v[2], (double)v[3]);
       }
       continue;
     }
     // 8 nodes per lane per round, all identity loads issued before the stores (a Dirichlet
     // line is a chain of dependent load -> store pairs otherwise)
     for (int a0 = lane; a0 < nnodes; a0 += 256) {
-      double v[8];
+      T v[8];
       int64_t gis[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -161,7 +180,7 @@ static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant_
                           ((d & 8u) && gy == Ny - 1) || ((d & 16u) && gz == 0) || ((d & 32u) && gz == Nz - 1);
         gis[j] = ((int64_t)gz * Ny + gy) * Nx + gx;
         const bool ident = a < nnodes && cons && !(P.skip_top_identity && gz == Nz - 1);
-        v[j] = ident ? __ldg(src + gis[j]) : 0.0;
+        v[j] = ident ? __ldg(src + gis[j]) : T(0);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -174,6 +193,31 @@ static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant_
 __device__ __forceinline__ void cp_async8z(double *smem, const double *gmem, unsigned src_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
+}
+// sizeof(T)-byte cp.async; `ok` false writes zeros without reading
+template <class T>
+__device__ __forceinline__ void cp_async_z(T *smem, const T *gmem, unsigned src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes ? 4u : 0u)
+                 : "memory");
+}
+// predicated reduction (at != 0) or plain store, no divergent branch
+__device__ __forceinline__ void red_or_st(double *p, double v, int at) {
+  asm volatile(
+      "{\n .reg .pred pa;\n setp.ne.s32 pa, %2, 0;\n"
+      " @pa red.global.add.f64 [%0], %1;\n @!pa st.global.f64 [%0], %1;\n}\n" ::"l"(p),
+      "d"(v), "r"(at)
+      : "memory");
+}
+__device__ __forceinline__ void red_or_st(float *p, float v, int at) {
+  asm volatile(
+      "{\n .reg .pred pa;\n setp.ne.s32 pa, %2, 0;\n"
+      " @pa red.global.add.f32 [%0], %1;\n @!pa st.global.f32 [%0], %1;\n}\n" ::"l"(p),
+      "f"(v), "r"(at)
+      : "memory");
 }
 
 // ---- host side -------------------------------------------------------------------
@@ -210,8 +254,17 @@ static inline void tile_params_common(const Geo &g, const Tables &t, int TX, int
     }
   to_eo(N, M, &P->M);
   to_eo(N, Kx, &P->K);
+  for (int i = 0; i < kMaxH; ++i)
+    for (int j = 0; j < kMaxH; ++j) {
+      P->Mf.E[i][j] = (float)P->M.E[i][j];
+      P->Mf.O[i][j] = (float)P->M.O[i][j];
+      P->Kf.E[i][j] = (float)P->K.E[i][j];
+      P->Kf.O[i][j] = (float)P->K.O[i][j];
+    }
   P->ry = g.fcart[1] / g.fcart[0];
   P->rz = g.fcart[2] / g.fcart[0];
+  P->ryf = (float)P->ry;
+  P->rzf = (float)P->rz;
   P->Nx = g.N[0];
   P->Ny = g.N[1];
   P->Nz = g.N[2];
@@ -287,8 +340,9 @@ __host__ __device__ inline void tile_chunk_layers(const TileParams &P, int c, in
 
 // init kernel: planes shared between blocks (internal tile edges, chunk planes)
 // get 0, Dirichlet faces get the identity value
+template <class T>
 static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, int K, int TX, int TY,
-                                           const double *src, double *dst, cudaStream_t s, int64_t *launches) {
+                                           const T *src, T *dst, cudaStream_t s, int64_t *launches) {
   PlaneSet ps;
   std::memset(&ps, 0, sizeof(ps));
   int total = 0;
@@ -319,7 +373,7 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
   ++*launches;
   for (int f = 0; f < ps.nfam; ++f) ps.total_lines += ps.lines[f];
   const int blocks = (int)std::min<int64_t>((ps.total_lines + 7) / 8, 148 * 8);
-  k_tile_init<<<blocks, 256, 0, s>>>(P, ps, src, dst);
+  k_tile_init<T><<<blocks, 256, 0, s>>>(P, ps, src, dst);
   return cudaGetLastError();
 }
 

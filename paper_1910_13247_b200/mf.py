@@ -56,7 +56,8 @@ class CGResultC(ctypes.Structure):
 
 class MGParams(ctypes.Structure):
     _fields_ = [("n_levels", ctypes.c_int32), ("max_coarse_dofs", ctypes.c_int64), ("smooth_degree", ctypes.c_int32),
-                ("smooth_range", ctypes.c_double), ("smooth_safety", ctypes.c_double), ("eig_cg_steps", ctypes.c_int32)]
+                ("smooth_range", ctypes.c_double), ("smooth_safety", ctypes.c_double), ("eig_cg_steps", ctypes.c_int32),
+                ("precision", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -71,7 +72,7 @@ EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_
            "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing",
            "mf_partition", "mf_mg_create", "mf_mg_destroy", "mf_mg_levels", "mf_mg_level_size", "mf_mg_level_op",
            "mf_mg_level_lambda", "mf_mg_prolongate", "mf_mg_restrict", "mf_mg_vcycle", "mf_mg_cg_solve",
-           "mf_mg_set_stream"]
+           "mf_mg_set_stream", "mf_apply_f32"]
 
 _lib = None
 
@@ -119,6 +120,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "mf_mg_cg_solve": [vp, vp, vp, i64, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(CGResultC), dp,
                            ctypes.c_int32],
         "mf_mg_set_stream": [vp, vp],
+        "mf_apply_f32": [vp, vp, i64, vp, i64],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -257,6 +259,18 @@ class Operator:
         _check(load().mf_apply(self._h, self._vec(src, "src"), src.numel(), self._vec(dst, "dst"), dst.numel()))
         return dst
 
+    def apply_f32(self, src, dst=None):
+        """The FP32 instance of the apply (mixed-precision multigrid); float32 CUDA tensors."""
+        t = self._torch
+        dst = t.zeros(self.n_local, dtype=t.float32, device=self.device) if dst is None else dst
+        for x, name in ((src, "src"), (dst, "dst")):
+            if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float32 and x.is_contiguous()):
+                raise TypeError(f"{name} must be a contiguous float32 CUDA tensor")
+        self._stream()
+        _check(load().mf_apply_f32(self._h, ctypes.c_void_p(src.data_ptr()), src.numel(),
+                                   ctypes.c_void_p(dst.data_ptr()), dst.numel()))
+        return dst
+
     def apply_host(self, src: np.ndarray, dst: np.ndarray | None = None) -> np.ndarray:
         src = np.ascontiguousarray(src, dtype=np.float64)
         dst = np.empty_like(src) if dst is None else dst
@@ -329,7 +343,7 @@ class Multigrid:
 
     def __init__(self, n_cells, degree, lower=None, upper=None, geometry="cartesian", eps=0.1, coeff=1.0,
                  dirichlet_faces=None, n_levels=0, max_coarse_dofs=1000, smooth_degree=6, smooth_range=20.0,
-                 smooth_safety=1.2, eig_cg_steps=12):
+                 smooth_safety=1.2, eig_cg_steps=12, precision="fp64"):
         import torch
 
         if not torch.cuda.is_available():
@@ -339,7 +353,8 @@ class Multigrid:
         m = make_mesh(n_cells, 3, lower, upper, geometry, eps, dirichlet_faces)
         c = Coeff()
         c.kind, c.value = (1, 0.0) if coeff == "variable" else (0, float(coeff))
-        prm = MGParams(n_levels, max_coarse_dofs, smooth_degree, smooth_range, smooth_safety, eig_cg_steps)
+        prm = MGParams(n_levels, max_coarse_dofs, smooth_degree, smooth_range, smooth_safety, eig_cg_steps,
+                       {"fp64": 0, "mixed": 1}[precision])
         h = ctypes.c_void_p()
         L = load()
         _check(L.mf_mg_create(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(prm), ctypes.byref(h)))

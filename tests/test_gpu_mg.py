@@ -108,3 +108,46 @@ def test_mg_errors(torch):
     M = Multigrid((4, 4, 4), 2, n_levels=2)
     with pytest.raises(TypeError):
         M.vcycle(M.new_vector(0))
+
+
+F32_CASES = [
+    dict(dim=3, n_cells=(9, 10, 11), k=2),
+    dict(dim=3, n_cells=(9, 17, 7), k=4, dirichlet=0b011001),
+    dict(dim=3, n_cells=(9, 9, 13), k=3, upper=(1.0, 2.0, 0.5), coeff=3.0),
+    dict(dim=3, n_cells=(5, 4, 6), k=3, geometry="sine", coeff="variable"),
+    dict(dim=3, n_cells=(3, 3, 2), k=5),
+    dict(dim=3, n_cells=(4, 3, 5), k=2, coeff="variable"),
+]
+
+
+@pytest.mark.parametrize("case", F32_CASES, ids=lambda c: f"k{c['k']}-{'x'.join(map(str, c['n_cells']))}")
+def test_apply_f32_matches_oracle_to_single_precision(case, torch):
+    # FP32 instance of the apply kernels (§8(f) f2): relative L2 error ~ (number of
+    # rounded FP32 operations per output) x 2^-24; bound 2e-6 (x, A fixed in FP64)
+    from tests._helpers import cuda_operator, oracle_problem
+
+    p = oracle_problem(case)
+    A = oracle.CSR(p)
+    op = cuda_operator(case)
+    x = seeded(A.n, 1).astype(np.float32)
+    y = op.apply_f32(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    assert rel_l2(y, A @ x.astype(np.float64)) <= 2e-6
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[4], dict(n_cells=(8, 8, 8), k=2), dict(n_cells=(4, 4, 4), k=4)],
+                         ids=_id)
+def test_mixed_precision_mg_pcg(case, torch):
+    # FP32 V-cycle inside the FP64 CG: the FP64 residual still reaches
+    # 1e-10, within a couple of iterations of the FP64 V-cycle, same solution
+    from paper_1910_13247_b200 import Multigrid
+
+    M64, H = _pair(case, torch)
+    M32 = Multigrid(case["n_cells"], case["k"], upper=case.get("upper"), geometry=case.get("geometry", "cartesian"),
+                    coeff=case.get("coeff", 1.0), dirichlet_faces=case.get("dirichlet"), n_levels=M64.n_levels,
+                    precision="mixed")
+    b = oracle.rhs(H.levels[-1].p, 0)
+    ref = mg.mg_pcg(H, b, 1e-10)
+    x, res = M32.cg_solve(torch.from_numpy(b).cuda(), rel_tol=1e-10)
+    assert res.final_rel_residual <= 1e-10
+    assert res.iterations <= ref.iterations + 2
+    assert rel_l2(x.cpu().numpy(), ref.x) <= 1e-8
