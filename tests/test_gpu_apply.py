@@ -222,3 +222,44 @@ def test_cfg4_full_size_sampled_rows(torch):
     rows = np.concatenate([rng.choice(op.n_local, 300, replace=False), [0, op.n_local - 1, op.n_local // 2]])
     ref = oracle.apply_rows(p, rows, x)
     assert np.abs(y[rows] - ref).max() <= CUDA_ORACLE_TOL * np.abs(ref).max()
+
+
+def _one_d(k, n, which):
+    # global 1D stiffness (which=0) / mass (which=1) on [0,1] from the oracle, no constraints
+    return oracle.CSR(oracle.problem(dim=1, n_cells=(n,), degree=k), which=which, dirichlet=False).dense()
+
+
+@pytest.mark.parametrize("cfg", [((256, 256, 256), 4), ((256, 256, 256), 6)], ids=["cfg5q4", "cfg5q6"])
+def test_full_size_separable_input(cfg, torch):
+    # BASELINE configs[4] sizes on ONE GPU (1.08 / 3.63 billion DoFs; 64-bit indexing):
+    # x = a (x) b (x) c with a, b, c vanishing at the ends, so on the brick
+    # A x = (K a)(M b)(M c) + (M a)(K b)(M c) + (M a)(M b)(K c) with the oracle's 1D
+    # matrices (the Kronecker identity is pinned in tests/test_oracle_operator.py);
+    # checked row by row at sampled DoFs, and over all DoFs with torch outer products
+    (nc, k) = cfg
+    n1 = k * nc[0] + 1
+    K1, M1 = _one_d(k, nc[0], 0), _one_d(k, nc[0], 1)
+    v = [seeded(n1, s) for s in (21, 22, 23)]
+    for w in v:
+        w[0] = w[-1] = 0.0
+    Kv, Mv = [K1 @ w for w in v], [M1 @ w for w in v]
+    for w in Kv + Mv:  # Dirichlet rows are identity rows and x vanishes there
+        w[0] = w[-1] = 0.0
+    op = cuda_operator(dict(dim=3, n_cells=nc, k=k))
+    assert op.n_local == n1 ** 3
+    g = [torch.from_numpy(w).cuda() for w in v]
+    x = torch.einsum("k,j,i->kji", g[2], g[1], g[0]).reshape(-1)  # z slowest, x fastest
+    y = op.apply(x)
+    del x
+    rows = np.random.default_rng(2).integers(0, op.n_local, 300)
+    yr = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    i, j, kk = rows % n1, (rows // n1) % n1, rows // (n1 * n1)
+    ref = Kv[0][i] * Mv[1][j] * Mv[2][kk] + Mv[0][i] * Kv[1][j] * Mv[2][kk] + Mv[0][i] * Mv[1][j] * Kv[2][kk]
+    scale = np.abs(ref).max()
+    assert np.abs(yr - ref).max() <= CUDA_ORACLE_TOL * scale
+    t = [torch.from_numpy(a).cuda() for a in (Kv[0], Mv[0], Kv[1], Mv[1], Kv[2], Mv[2])]
+    exp = torch.einsum("k,j,i->kji", t[5], t[3], t[0]).reshape(-1)
+    exp += torch.einsum("k,j,i->kji", t[5], t[2], t[1]).reshape(-1)
+    exp += torch.einsum("k,j,i->kji", t[4], t[3], t[1]).reshape(-1)
+    err = ((y - exp).norm() / exp.norm()).item()
+    assert err <= CUDA_ORACLE_TOL, err
