@@ -24,6 +24,10 @@ struct Tables {
   double w[kMaxN];
   double gll[kMaxN];
   double xi[kMaxN];
+  // reference 1D mass M = S^T W S and stiffness K = D^T W D on [0,1] (Gauss(k+1) is
+  // exact for both): the Kronecker form of the Cartesian constant-coefficient operator
+  double Mr[kMaxN][kMaxN];
+  double Kr[kMaxN][kMaxN];
 };
 
 // Host-side construction (tables.cpp): an implementation of the 1D rules

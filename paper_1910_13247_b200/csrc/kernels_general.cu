@@ -123,6 +123,8 @@ struct TablesF {
   float Co[kMaxN][kMaxN];
   float w[kMaxN];
   float xi[kMaxN];
+  float Mr[kMaxN][kMaxN];
+  float Kr[kMaxN][kMaxN];
 };
 template <class T>
 struct TabOf;
@@ -523,6 +525,78 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
   const CellInfo ci = cell_info<3, K>(g, valid ? cell : ncells, ncells);
   T a[N], b[N];
 
+  if constexpr (GEOM == 0) {
+    // Cartesian box, constant coefficient: the Gauss(k+1)-exact Kronecker form of the
+    // cell operator, 7 one-dimensional products instead of 12
+    // sweeps and no quadrature-point pass:
+    //   v = fx K(x) M(y) M(z) u + fy M K M u + fz M M K u,   M, K = reference 1D mass / stiffness
+    //   z-pencils: a = M u, b = fz K u;  y-pencils: c = M a, d = fy K a, e = M b;
+    //   x-pencils: v = fx K c + M (d + e)
+    const T fx = (T)g.fcart[0], fy = (T)g.fcart[1], fz = (T)g.fcart[2];
+    T *A1 = G0, *B1 = G1;
+    if (active) {  // gather the x-pencil
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        int64_t gi;
+        bool cons, owner;
+        node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
+        a[i] = (valid && !cons) ? __ldg(src + gi) : T(0);
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) U[o0[i]] = a[i];
+    }
+    __syncthreads();
+    if (active) {  // z
+#pragma unroll
+      for (int i = 0; i < N; ++i) a[i] = U[o2[i]];
+      mat1d<N, false>(t.Mr, a, b);
+#pragma unroll
+      for (int i = 0; i < N; ++i) A1[o2[i]] = b[i];
+      mat1d<N, false>(t.Kr, a, b);
+#pragma unroll
+      for (int i = 0; i < N; ++i) B1[o2[i]] = fz * b[i];
+    }
+    __syncthreads();
+    if (active) {  // y (each thread rewrites only its own pencil's slots)
+#pragma unroll
+      for (int i = 0; i < N; ++i) a[i] = A1[o1[i]];
+      mat1d<N, false>(t.Mr, a, b);
+#pragma unroll
+      for (int i = 0; i < N; ++i) A1[o1[i]] = b[i];
+      mat1d<N, false>(t.Kr, a, b);
+#pragma unroll
+      for (int i = 0; i < N; ++i) U[o1[i]] = fy * b[i];
+#pragma unroll
+      for (int i = 0; i < N; ++i) a[i] = B1[o1[i]];
+      mat1d<N, false>(t.Mr, a, b);
+#pragma unroll
+      for (int i = 0; i < N; ++i) B1[o1[i]] = b[i];
+    }
+    __syncthreads();
+    if (active && valid) {  // x, then scatter-add and identity rows
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        a[i] = A1[o0[i]];
+        gz[i] = U[o0[i]] + B1[o0[i]];
+      }
+      mat1d<N, false>(t.Kr, a, b);
+      T v[N];
+      mat1d<N, false>(t.Mr, gz, v);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        int64_t gi;
+        bool cons, owner;
+        node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
+        if (cons) {
+          if (owner) dst[gi] = __ldg(src + gi);
+        } else {
+          atomicAdd(dst + gi, fma(fx, b[i], v[i]));
+        }
+      }
+    }
+    return;
+  }
+
   // 1: gather the x-pencil (y = p % N, z = p / N), S along x
   if (active) {
 #pragma unroll
@@ -760,6 +834,10 @@ cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float 
     }
     tf.w[i] = (float)t.w[i];
     tf.xi[i] = (float)t.xi[i];
+    for (int j = 0; j < kMaxN; ++j) {
+      tf.Mr[i][j] = (float)t.Mr[i][j];
+      tf.Kr[i][j] = (float)t.Kr[i][j];
+    }
   }
   ++*launches;
   const int gk = geom_kind(g);

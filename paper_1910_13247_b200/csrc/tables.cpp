@@ -121,6 +121,21 @@ void build_tables(int k, Tables *t) {
       t->D[q][i] = (double)d;
     }
   }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      ld mm = 0.0L, kk = 0.0L;
+      for (int q = 0; q < n; ++q) {
+        ld di = 0.0L, dj = 0.0L;
+        for (int p = 0; p < n; ++p) {
+          di += Co[q][p] * S[p][i];
+          dj += Co[q][p] * S[p][j];
+        }
+        mm += wg[q] * S[q][i] * S[q][j];
+        kk += wg[q] * di * dj;
+      }
+      t->Mr[i][j] = (double)mm;
+      t->Kr[i][j] = (double)kk;
+    }
 }
 
 }  // namespace mf
