@@ -28,6 +28,10 @@ struct Tables {
   // exact for both): the Kronecker form of the Cartesian constant-coefficient operator
   double Mr[kMaxN][kMaxN];
   double Kr[kMaxN][kMaxN];
+  // their even-odd parts (both are centro-symmetric): rows i < (n+1)/2 of E act on
+  // e_j = u_j + u_{n-1-j} (j < n/2; e_{n/2} = u_{n/2} for odd n), rows i < n/2 of O on
+  // o_j = u_j - u_{n-1-j}; v_i = ve_i + vo_i, v_{n-1-i} = ve_i - vo_i, v_{n/2} = ve_{n/2}
+  double Me[5][5], Mo[5][5], Ke[5][5], Ko[5][5];
 };
 
 // Host-side construction (tables.cpp): an implementation of the 1D rules

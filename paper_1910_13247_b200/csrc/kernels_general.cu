@@ -125,7 +125,39 @@ struct TablesF {
   float xi[kMaxN];
   float Mr[kMaxN][kMaxN];
   float Kr[kMaxN][kMaxN];
+  float Me[5][5], Mo[5][5], Ke[5][5], Ko[5][5];
 };
+
+// even-odd 1D product with the centro-symmetric matrix (E, O) (see Tables::Me)
+template <int N, class T>
+__device__ __forceinline__ void eo_sp(const T *u, T *e, T *o) {
+  constexpr int m = N / 2;
+#pragma unroll
+  for (int j = 0; j < m; ++j) {
+    e[j] = u[j] + u[N - 1 - j];
+    o[j] = u[j] - u[N - 1 - j];
+  }
+  if (N & 1) e[m] = u[m];
+}
+template <int N, class T>
+__device__ __forceinline__ void eo_mv(const T (&E)[5][5], const T (&O)[5][5], const T *e, const T *o, T *v) {
+  constexpr int m = N / 2, h = (N + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < h; ++i) {
+    T ve = E[i][0] * e[0];
+#pragma unroll
+    for (int j = 1; j < h; ++j) ve = fma(E[i][j], e[j], ve);
+    if (i < m) {
+      T vo = O[i][0] * o[0];
+#pragma unroll
+      for (int j = 1; j < m; ++j) vo = fma(O[i][j], o[j], vo);
+      v[i] = ve + vo;
+      v[N - 1 - i] = ve - vo;
+    } else {
+      v[i] = ve;
+    }
+  }
+}
 template <class T>
 struct TabOf;
 template <>
@@ -546,13 +578,16 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
       for (int i = 0; i < N; ++i) U[o0[i]] = a[i];
     }
     __syncthreads();
+    constexpr int h = (N + 1) / 2;
+    T e[h], o[h];  // even-odd parts of the pencil (M and K are centro-symmetric)
     if (active) {  // z
 #pragma unroll
       for (int i = 0; i < N; ++i) a[i] = U[o2[i]];
-      mat1d<N, false>(t.Mr, a, b);
+      eo_sp<N>(a, e, o);
+      eo_mv<N>(t.Me, t.Mo, e, o, b);
 #pragma unroll
       for (int i = 0; i < N; ++i) A1[o2[i]] = b[i];
-      mat1d<N, false>(t.Kr, a, b);
+      eo_mv<N>(t.Ke, t.Ko, e, o, b);
 #pragma unroll
       for (int i = 0; i < N; ++i) B1[o2[i]] = fz * b[i];
     }
@@ -560,15 +595,17 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
     if (active) {  // y (each thread rewrites only its own pencil's slots)
 #pragma unroll
       for (int i = 0; i < N; ++i) a[i] = A1[o1[i]];
-      mat1d<N, false>(t.Mr, a, b);
+      eo_sp<N>(a, e, o);
+      eo_mv<N>(t.Me, t.Mo, e, o, b);
 #pragma unroll
       for (int i = 0; i < N; ++i) A1[o1[i]] = b[i];
-      mat1d<N, false>(t.Kr, a, b);
+      eo_mv<N>(t.Ke, t.Ko, e, o, b);
 #pragma unroll
       for (int i = 0; i < N; ++i) U[o1[i]] = fy * b[i];
 #pragma unroll
       for (int i = 0; i < N; ++i) a[i] = B1[o1[i]];
-      mat1d<N, false>(t.Mr, a, b);
+      eo_sp<N>(a, e, o);
+      eo_mv<N>(t.Me, t.Mo, e, o, b);
 #pragma unroll
       for (int i = 0; i < N; ++i) B1[o1[i]] = b[i];
     }
@@ -579,9 +616,11 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
         a[i] = A1[o0[i]];
         gz[i] = U[o0[i]] + B1[o0[i]];
       }
-      mat1d<N, false>(t.Kr, a, b);
+      eo_sp<N>(a, e, o);
+      eo_mv<N>(t.Ke, t.Ko, e, o, b);
       T v[N];
-      mat1d<N, false>(t.Mr, gz, v);
+      eo_sp<N>(gz, e, o);
+      eo_mv<N>(t.Me, t.Mo, e, o, v);
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         int64_t gi;
@@ -837,6 +876,14 @@ cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float 
     for (int j = 0; j < kMaxN; ++j) {
       tf.Mr[i][j] = (float)t.Mr[i][j];
       tf.Kr[i][j] = (float)t.Kr[i][j];
+    }
+  }
+  for (int i = 0; i < 5; ++i) {
+    for (int j = 0; j < 5; ++j) {
+      tf.Me[i][j] = (float)t.Me[i][j];
+      tf.Mo[i][j] = (float)t.Mo[i][j];
+      tf.Ke[i][j] = (float)t.Ke[i][j];
+      tf.Ko[i][j] = (float)t.Ko[i][j];
     }
   }
   ++*launches;

@@ -136,6 +136,19 @@ void build_tables(int k, Tables *t) {
       t->Mr[i][j] = (double)mm;
       t->Kr[i][j] = (double)kk;
     }
+  const int m = n / 2, h = (n + 1) / 2;
+  auto eo = [&](const double A[kMaxN][kMaxN], double E[5][5], double O[5][5]) {
+    for (int i = 0; i < h; ++i) {
+      for (int j = 0; j < m; ++j) E[i][j] = 0.5 * (A[i][j] + A[i][n - 1 - j]);
+      if (n & 1) E[i][m] = A[i][m];
+    }
+    if (n & 1)
+      for (int j = 0; j < m; ++j) E[m][j] = A[m][j];
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) O[i][j] = 0.5 * (A[i][j] - A[i][n - 1 - j]);
+  };
+  eo(t->Mr, t->Me, t->Mo);
+  eo(t->Kr, t->Ke, t->Ko);
 }
 
 }  // namespace mf
