@@ -87,6 +87,17 @@ mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff,
 void mf_destroy(mf_op *op);
 const char *mf_last_error(void);
 
+/* The symmetric interior penalty DG Laplacian on the same brick (
+ * PAPER.md P:1360-1364 §6.1 "symmetric interior penalty discontinuous Galerkin"):
+ * discontinuous Q_k Lagrange on the GLL nodes of each cell, DoF index = cell (k+1)^3 +
+ * local (both x-fastest), Gauss(k+1) on cells and faces, penalty 2 (k+1)^2 / h_n,
+ * weak (Nitsche) homogeneous Dirichlet on every face (R16-R18).  3D,
+ * Cartesian geometry, constant coefficient, dirichlet_faces = all six, one rank
+ * (else MF_ERR_ARGUMENT).  The returned op works with mf_apply, mf_diagonal,
+ * mf_estimate_lambda_max, mf_chebyshev and mf_cg_solve (no constrained DoFs;
+ * mf_get_info reports apply_variant 4). */
+mf_status mf_create_dg(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff, mf_op **out);
+
 /* NCCL unique id (128 bytes) for mf_dist, created on rank 0 and broadcast by the caller. */
 mf_status mf_nccl_unique_id(uint8_t *out128);
 

@@ -37,6 +37,7 @@ struct mf_op {
   // halo overlap (§8(e)): the boundary cell layers first, the NCCL exchange of the shared
   // planes on comm_stream while the interior layers run on stream
   bool zsplit = false;  // world > 1, or MF_ZSPLIT=1 (the same launch sequence on one GPU)
+  bool dg = false;      // discontinuous (SIP) discretization, mf_create_dg
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   // live kernel timing (mf_set_kernel_timing)
@@ -253,6 +254,24 @@ extern "C" void mf_destroy(mf_op *op) {
   delete op;
 }
 
+// DG-SIP operator: the same brick, discontinuous Q_k on the GLL nodes
+// of each cell, DoFs cell-major; weak (Nitsche) Dirichlet on every face
+extern "C" mf_status mf_create_dg(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff, mf_op **out) {
+  if (!mesh || !coeff || !out) return fail(MF_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (mesh->dim != 3 || mesh->geometry != MF_GEOM_CARTESIAN || coeff->kind != MF_COEFF_CONSTANT)
+    return fail(MF_ERR_ARGUMENT, "DG: 3D Cartesian brick with a constant coefficient");
+  if ((mesh->dirichlet_faces & 63u) != 63u) return fail(MF_ERR_ARGUMENT, "DG: weak Dirichlet on all six faces");
+  mf_op *op = nullptr;
+  STATUS_TRY(mf_create(mesh, degree, coeff, nullptr, &op));
+  const Geo &g = op->g;
+  op->dg = true;
+  op->first_global = 0;
+  op->n_local = op->n_global = op->n_owned = g.nc[0] * g.nc[1] * g.nc[2] * ipow(degree + 1, 3);
+  *out = op;
+  return MF_OK;
+}
+
 extern "C" mf_status mf_sizes(const mf_op *op, int64_t *n_local, int64_t *first_global, int64_t *n_global,
                               int64_t *n_owned) {
   if (!op) return fail(MF_ERR_ARGUMENT, "null op");
@@ -359,6 +378,11 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
 }
 
 static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
+  if (op->dg) {
+    STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_apply_dg(op->g, op->t, src, dst, op->stream, &op->launches));
+    return timing_mark(op);
+  }
   const int var = chosen_variant(op);
   if (op->zsplit && op->g.dim == 3 && var != kVariantCartTile) return apply_split(op, src, dst, var);
   if (var == kVariantCartTile) {
@@ -423,6 +447,10 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
 }
 
 static mf_status diagonal_impl(mf_op *op, double *diag) {
+  if (op->dg) {
+    CUDA_TRY(launch_diagonal_dg(op->g, op->t, diag, op->stream, &op->launches));
+    return MF_OK;
+  }
   CUDA_TRY(launch_zero(diag, op->n_local, op->stream, &op->launches));
   CUDA_TRY(launch_diagonal(op->g, op->t, diag, op->metric, op->stream, &op->launches));
   return halo_exchange(op, diag);
@@ -488,7 +516,7 @@ static mf_status lambda_impl(mf_op *op, int steps, double *lam) {
   cudaStream_t s = op->stream;
   double *r = op->r, *z = op->z, *p = op->p, *v = op->v;
   CUDA_TRY(launch_splitmix(r, n, op->first_global, 0, s, &op->launches));
-  CUDA_TRY(launch_set_constrained(op->g, r, 0.0, s, &op->launches));
+  if (!op->dg) CUDA_TRY(launch_set_constrained(op->g, r, 0.0, s, &op->launches));  // (DG: no constrained DoFs)
   CUDA_TRY(launch_mul(op->dinv, r, z, n, s, &op->launches));
   CUDA_TRY(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   {
@@ -577,7 +605,7 @@ static mf_status ensure_f32(mf_op *op) {
 }
 
 mf_status apply_f32(mf_op *op, const float *src, float *dst) {
-  if (op->world != 1 || op->g.dim != 3) return fail(MF_ERR_ARGUMENT, "FP32 apply: 3D, one rank");
+  if (op->world != 1 || op->g.dim != 3 || op->dg) return fail(MF_ERR_ARGUMENT, "FP32 apply: 3D CG, one rank");
   STATUS_TRY(ensure_f32(op));
   if (chosen_variant(op) == kVariantCartPlane) {
     CUDA_TRY(launch_apply_cart_plane_f32(op->g, op->t, src, dst, op->stream, &op->launches));
@@ -711,7 +739,7 @@ extern "C" mf_status mf_get_info(const mf_op *op, mf_info *info) {
   info->degree = g.k;
   info->geometry = g.geom;
   info->coeff_kind = g.coeff_kind;
-  info->apply_variant = chosen_variant(op);
+  info->apply_variant = op->dg ? 4 : chosen_variant(op);
   info->n_cells_local = ncells_local(g);
   info->kernel_launches = op->launches;
   const int64_t nq = ipow(g.k + 1, g.dim);

@@ -80,6 +80,10 @@ cudaError_t launch_apply_cart_plane_f32(const Geo &g, const Tables &t, const flo
 cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float *src, float *dst,
                                      const float *metric, cudaStream_t s, int64_t *launches);
 bool cart_plane_supported(const Geo &g);
+// DG-SIP operator and its diagonal (kernels_dg.cu, §8(f) f4)
+cudaError_t launch_apply_dg(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+                            int64_t *launches);
+cudaError_t launch_diagonal_dg(const Geo &g, const Tables &t, double *diag, cudaStream_t s, int64_t *launches);
 cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
                           int64_t *launches);
 cudaError_t launch_diagonal(const Geo &g, const Tables &t, double *diag, const double *metric,

@@ -72,7 +72,7 @@ EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_
            "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing",
            "mf_partition", "mf_mg_create", "mf_mg_destroy", "mf_mg_levels", "mf_mg_level_size", "mf_mg_level_op",
            "mf_mg_level_lambda", "mf_mg_prolongate", "mf_mg_restrict", "mf_mg_vcycle", "mf_mg_cg_solve",
-           "mf_mg_set_stream", "mf_apply_f32"]
+           "mf_mg_set_stream", "mf_apply_f32", "mf_create_dg"]
 
 _lib = None
 
@@ -121,6 +121,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
                            ctypes.c_int32],
         "mf_mg_set_stream": [vp, vp],
         "mf_apply_f32": [vp, vp, i64, vp, i64],
+        "mf_create_dg": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.POINTER(Coeff), ctypes.POINTER(vp)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -179,7 +180,7 @@ class Operator:
     [first_global, first_global + n_local) of the x-fastest global vector)."""
 
     def __init__(self, n_cells, degree, dim=None, lower=None, upper=None, geometry="cartesian", eps=0.1,
-                 coeff=1.0, dirichlet_faces=None, group=None, device=None):
+                 coeff=1.0, dirichlet_faces=None, group=None, device=None, discretization="cg"):
         import torch
 
         if not torch.cuda.is_available():
@@ -225,7 +226,10 @@ class Operator:
             dist.rank, dist.world_size = 0, 1
         with torch.cuda.device(device):
             h = ctypes.c_void_p()
-            _check(L.mf_create(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(dist), ctypes.byref(h)))
+            if discretization == "dg":  # symmetric interior penalty DG (mf_create_dg)
+                _check(L.mf_create_dg(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(h)))
+            else:
+                _check(L.mf_create(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(dist), ctypes.byref(h)))
         self._h = h
         self.dim, self.degree, self.mesh = dim, degree, m
         a, b, cc, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
