@@ -71,7 +71,11 @@ __global__ void __launch_bounds__(256) k_apply_dg(const __grid_constant__ DGPara
   const bool active = cl < cpb;
   const int64_t cell = (int64_t)blockIdx.x * cpb + cl;
   const bool valid = active && cell < ncells;
-  double *U = sm + (active ? cl : 0) * 3 * NV, *T = U + NV, *W = T + NV;
+  // shared memory: the contiguous cells [cell0 - 1, cell0 + cpb] (own cells and their
+  // x-neighbours, one coalesced load), then T and W per cell
+  const int64_t cell0 = (int64_t)blockIdx.x * cpb;
+  double *Ux = sm, *U = Ux + (cl + 1) * NV;
+  double *T = sm + (cpb + 2) * NV + (active ? cl : 0) * 2 * NV, *W = T + NV;
   int64_t c[3] = {0, 0, 0};
   if (valid) {
     c[0] = cell % D.nc[0];
@@ -82,9 +86,12 @@ __global__ void __launch_bounds__(256) k_apply_dg(const __grid_constant__ DGPara
   const int64_t stride[3] = {1, D.nc[0], D.nc[0] * D.nc[1]};
   const double *uK = src + cell * NV;
   double a[N], b[N];
-  if (valid) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) U[N * p + i] = __ldg(uK + N * p + i);
+  {
+    const int64_t g0 = (cell0 - 1) * NV, gend = ncells * NV;
+    for (int idx = threadIdx.x; idx < (cpb + 2) * NV; idx += blockDim.x) {
+      const int64_t gi = g0 + idx;
+      if (gi >= 0 && gi < gend) Ux[idx] = __ldg(src + gi);
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -95,16 +102,16 @@ __global__ void __launch_bounds__(256) k_apply_dg(const __grid_constant__ DGPara
 #pragma unroll
       for (int i = 0; i < N; ++i) a[i] = U[slot<N>(e, p, i)];
       mv<N>(D.B[e][(lo ? 1 : 0) + (hi ? 2 : 0)], a, b);
-      if (!lo) {
+      if (!lo) {  // x: the previous cell is in shared memory
         const double *un = uK - stride[e] * NV;
 #pragma unroll
-        for (int i = 0; i < N; ++i) a[i] = __ldg(un + slot<N>(e, p, i));
+        for (int i = 0; i < N; ++i) a[i] = e == 0 ? U[slot<N>(e, p, i) - NV] : __ldg(un + slot<N>(e, p, i));
         mv_acc<N>(D.B[e][4], a, b);
       }
       if (!hi) {
         const double *un = uK + stride[e] * NV;
 #pragma unroll
-        for (int i = 0; i < N; ++i) a[i] = __ldg(un + slot<N>(e, p, i));
+        for (int i = 0; i < N; ++i) a[i] = e == 0 ? U[slot<N>(e, p, i) + NV] : __ldg(un + slot<N>(e, p, i));
         mv_acc<N>(D.B[e][5], a, b);
       }
 #pragma unroll
@@ -220,9 +227,9 @@ template <int K>
 cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaStream_t s) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   int cpb = 256 / NP;
-  while (cpb > 1 && cpb * 3 * NV * 8 > 96 * 1024) --cpb;
+  while (cpb > 1 && (3 * cpb + 2) * NV * 8 > 96 * 1024) --cpb;
   if (cpb < 1) cpb = 1;
-  const size_t smem = (size_t)cpb * 3 * NV * sizeof(double);
+  const size_t smem = (size_t)(3 * cpb + 2) * NV * sizeof(double);  // own + x-neighbour cells, T, W
   static bool attr = (cudaFuncSetAttribute(k_apply_dg<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
                       true);
   (void)attr;
