@@ -49,6 +49,22 @@ def load_traffic(config):
         return None
 
 
+FP64_PEAK_TINSTR = 57.47 * 148 * 1.965e9 / 1e12  # measured DFMA issue rate (profiles/r01_microbench.json)
+
+
+def fp64_roofline(config, n_dofs, kernel_ms):
+    """FP64-pipe view of the same region: ncu-counted FP64 instructions per DoF
+    (profiles/traffic.json) over the live kernel time, against the measured DFMA rate."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            ipd = json.load(f)[config]["fp64_instr_per_dof"]
+    except Exception:
+        return None
+    achieved = ipd * n_dofs / (kernel_ms * 1e-3) / 1e12
+    return {"instr_per_dof": ipd, "achieved": achieved, "peak": FP64_PEAK_TINSTR, "unit": "T FP64 instr/s",
+            "frac": achieved / FP64_PEAK_TINSTR}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -329,7 +345,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(args.config), "peak_kind": peak_kind,
                          "bytes_per_launch": bytes_per_launch, "kernel_ms": kern_avg_ms,
-                         "kernel_share_of_step": kern_avg_ms / ms_per_step},
+                         "kernel_share_of_step": kern_avg_ms / ms_per_step,
+                         "fp64": fp64_roofline(args.config, op.n_global, kern_avg_ms)},
             "e2e": {"value": e2e_val, "unit": "DoFs/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "steps": e2e_steps},
             "gpu_launches": launches,
