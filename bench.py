@@ -346,7 +346,7 @@ def main():
                          "frac": achieved / peak, "traffic": load_traffic(args.config), "peak_kind": peak_kind,
                          "bytes_per_launch": bytes_per_launch, "kernel_ms": kern_avg_ms,
                          "kernel_share_of_step": kern_avg_ms / ms_per_step,
-                         "fp64": fp64_roofline(args.config, op.n_global, kern_avg_ms)},
+                         "fp64": fp64_roofline(args.config, op.n_local, kern_avg_ms)},
             "e2e": {"value": e2e_val, "unit": "DoFs/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "steps": e2e_steps},
             "gpu_launches": launches,
