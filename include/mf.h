@@ -245,6 +245,24 @@ mf_status mf_mg_cg_solve(mf_mg *mg, const double *b, double *x, int64_t n, doubl
                          mf_cg_result *result, double *history, int32_t history_cap);
 mf_status mf_mg_set_stream(mf_mg *mg, void *cuda_stream);
 
+/* ---- Hanging nodes (restricted to one 2:1 interface; PAPER.md
+ * P:776-781 §3.5 "hanging node constraints"): the box [lower, upper] cut at
+ * z = z_mid into a coarse lower brick of n_cells_coarse cells and an upper brick
+ * refined once more (2 nx, 2 ny, nz_fine cells), Q_k on both, constant coefficient,
+ * Dirichlet (identity rows) on every outer face.  The fine interface nodes hang:
+ * u_f = (P_y (x) P_x) u_c on the interface (coarse face function interpolated at the
+ * fine nodes), applied in the gather and transposed in the scatter of the matrix-free
+ * apply.  Global vector (R20): every coarse-grid node (x-fastest, plane by
+ * plane), then the fine grid's nodes above the interface plane; n = nC + nF - one
+ * fine plane.  Device buffers of n doubles; asynchronous on the stream; single GPU. */
+typedef struct mf_hng mf_hng;
+mf_status mf_hng_create(const double *lower3, const double *upper3, double z_mid, const int64_t *n_cells_coarse3,
+                        int64_t nz_fine, int32_t degree, const mf_coeff *coeff, mf_hng **out);
+void mf_hng_destroy(mf_hng *h);
+mf_status mf_hng_sizes(const mf_hng *h, int64_t *n, int64_t *n_coarse);
+mf_status mf_hng_apply(mf_hng *h, const double *src, int64_t n_src, double *dst, int64_t n_dst);
+mf_status mf_hng_set_stream(mf_hng *h, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -557,3 +557,139 @@ extern "C" mf_status mf_mg_set_stream(mf_mg *mg, void *cuda_stream) {
   for (mf_op *op : mg->ops) MG_TRY(mf_set_stream(op, cuda_stream));
   return MF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Hanging nodes (restricted): the two-block mesh of a coarse lower
+// brick and a once-refined upper brick meeting at z = z_mid (R20).  The fine
+// interface nodes hang; continuity makes them the coarse face function interpolated at
+// the fine nodes, u_f(plane 0) = (P_y (x) P_x) u_c(top plane), so the matrix-free apply
+// is the gather/scatter of the constraint around the two block operators:
+//   y_c = A_c x_c;   x_f = [P2D x_c(top) | x(fine part)];   y_f = A_f x_f;
+//   y(fine part) = y_f(planes >= 1);   y_c(top) += P2D^T y_f(plane 0)
+// (coarse Dirichlet lines of the top plane masked on both sides, the identity rows of
+// either block kept).
+struct mf_hng {
+  mf_op *oc = nullptr, *of = nullptr;
+  Dims dc{}, df{};  // node counts of the two grids
+  int64_t nC = 0, nF = 0, n = 0, pc_n = 0, pf_n = 0;  // pc_n / pf_n: coarse / fine plane sizes
+  InterpT<double> I;
+  double *xf = nullptr, *yf = nullptr, *t1 = nullptr, *t2 = nullptr, *pc = nullptr;
+  cudaStream_t stream = 0;
+  int64_t launches = 0;
+};
+
+extern "C" void mf_hng_destroy(mf_hng *h) {
+  if (!h) return;
+  for (double *p : {h->xf, h->yf, h->t1, h->t2, h->pc}) cudaFree(p);
+  mf_destroy(h->oc);
+  mf_destroy(h->of);
+  delete h;
+}
+
+extern "C" mf_status mf_hng_create(const double *lower, const double *upper, double z_mid,
+                                   const int64_t *n_cells_coarse, int64_t nz_fine, int32_t degree,
+                                   const mf_coeff *coeff, mf_hng **out) {
+  if (!lower || !upper || !n_cells_coarse || !coeff || !out) return mf_set_error(MF_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (!(lower[2] < z_mid && z_mid < upper[2]) || nz_fine < 1 || coeff->kind != MF_COEFF_CONSTANT)
+    return mf_set_error(MF_ERR_ARGUMENT, "hanging nodes: lower z < z_mid < upper z, nz_fine >= 1, constant coefficient");
+  mf_mesh mc{}, mfm{};
+  mc.dim = mfm.dim = 3;
+  for (int e = 0; e < 3; ++e) {
+    mc.n_cells[e] = n_cells_coarse[e];
+    mc.lower[e] = mfm.lower[e] = lower[e];
+    mc.upper[e] = mfm.upper[e] = upper[e];
+  }
+  mc.upper[2] = z_mid;
+  mfm.lower[2] = z_mid;
+  mfm.n_cells[0] = 2 * n_cells_coarse[0];
+  mfm.n_cells[1] = 2 * n_cells_coarse[1];
+  mfm.n_cells[2] = nz_fine;
+  mc.geometry = mfm.geometry = MF_GEOM_CARTESIAN;
+  mc.dirichlet_faces = 0b011111u;   // x, y, bottom; the interface is natural
+  mfm.dirichlet_faces = 0b101111u;  // x, y, top
+  mf_hng *h = new mf_hng();
+  auto cleanup = [&](mf_status s) {
+    mf_hng_destroy(h);
+    return s;
+  };
+  mf_status st = mf_create(&mc, degree, coeff, nullptr, &h->oc);
+  if (st == MF_OK) st = mf_create(&mfm, degree, coeff, nullptr, &h->of);
+  if (st != MF_OK) return cleanup(st);
+  for (int e = 0; e < 3; ++e) {
+    h->dc.n[e] = degree * mc.n_cells[e] + 1;
+    h->df.n[e] = degree * mfm.n_cells[e] + 1;
+  }
+  h->pc_n = h->dc.n[0] * h->dc.n[1];
+  h->pf_n = h->df.n[0] * h->df.n[1];
+  h->nC = h->pc_n * h->dc.n[2];
+  h->nF = h->pf_n * h->df.n[2];
+  h->n = h->nC + h->nF - h->pf_n;
+  Tables tab;
+  build_tables(degree, &tab);
+  std::memset(&h->I, 0, sizeof(h->I));
+  h->I.k = degree;
+  for (int m = 0; m <= 2 * degree; ++m) {
+    const int child = m < degree ? 0 : (m < 2 * degree ? 1 : 2);
+    const double tm = child == 2 ? 1.0 : 0.5 * (child + tab.gll[m - child * degree]);
+    for (int j = 0; j <= degree; ++j) h->I.W[m][j] = lagrange(tab.gll, degree, j, tm);
+  }
+  if (cudaMalloc(&h->xf, h->nF * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->yf, h->nF * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->t1, h->pf_n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->t2, h->pf_n * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->pc, h->pc_n * sizeof(double)) != cudaSuccess)
+    return cleanup(mf_set_error(MF_ERR_OUT_OF_MEMORY, "hanging-node buffers"));
+  *out = h;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_hng_sizes(const mf_hng *h, int64_t *n, int64_t *n_coarse) {
+  if (!h) return mf_set_error(MF_ERR_ARGUMENT, "null argument");
+  if (n) *n = h->n;
+  if (n_coarse) *n_coarse = h->nC;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_hng_set_stream(mf_hng *h, void *cuda_stream) {
+  if (!h) return mf_set_error(MF_ERR_ARGUMENT, "null argument");
+  h->stream = (cudaStream_t)cuda_stream;
+  MG_TRY(mf_set_stream(h->oc, cuda_stream));
+  return mf_set_stream(h->of, cuda_stream);
+}
+
+extern "C" mf_status mf_hng_apply(mf_hng *h, const double *src, int64_t n_src, double *dst, int64_t n_dst) {
+  if (!h || !src || !dst) return mf_set_error(MF_ERR_ARGUMENT, "null argument");
+  if (n_src != h->n || n_dst != h->n) return mf_set_error(MF_ERR_LENGTH, "vector length != n");
+  if (src == dst) return mf_set_error(MF_ERR_ARGUMENT, "src and dst must be distinct");
+  cudaStream_t s = h->stream;
+  const Dims dp{{h->dc.n[0], h->dc.n[1], 1}};  // the coarse interface plane
+  const uint32_t lines = 0b1111u;              // its Dirichlet lines (x and y faces)
+  // coarse block
+  MG_TRY(mf_apply(h->oc, src, h->nC, dst, h->nC));
+  // gather: fine grid input = [P2D (masked coarse top plane) | fine part]
+  MG_CUDA(cudaMemcpyAsync(h->pc, src + h->nC - h->pc_n, h->pc_n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  k_zero_constrained<double><<<grid_for(h->pc_n), 256, 0, s>>>(h->pc, dp, lines);
+  Dims d1 = dp;
+  d1.n[0] = 2 * dp.n[0] - 1;
+  k_interp_axis<double><<<grid_for(d1.n[0] * d1.n[1]), 256, 0, s>>>(h->I, 0, dp, h->pc, h->t1);
+  k_interp_axis<double><<<grid_for(h->pf_n), 256, 0, s>>>(h->I, 1, d1, h->t1, h->xf);
+  MG_CUDA(cudaMemcpyAsync(h->xf + h->pf_n, src + h->nC, (h->nF - h->pf_n) * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s));
+  h->launches += 3;
+  // fine block
+  MG_TRY(mf_apply(h->of, h->xf, h->nF, h->yf, h->nF));
+  // scatter: fine part, and P2D^T of the interface plane into the coarse top plane
+  MG_CUDA(cudaMemcpyAsync(dst + h->nC, h->yf + h->pf_n, (h->nF - h->pf_n) * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s));
+  const Dims dfp{{h->df.n[0], h->df.n[1], 1}};
+  k_zero_constrained<double><<<grid_for(h->pf_n), 256, 0, s>>>(h->yf, dfp, lines);
+  k_restrict_axis<double><<<grid_for(d1.n[0] * d1.n[1]), 256, 0, s>>>(h->I, 1, d1, h->yf, h->t1);
+  k_restrict_axis<double><<<grid_for(h->pc_n), 256, 0, s>>>(h->I, 0, dp, h->t1, h->pc);
+  k_zero_constrained<double><<<grid_for(h->pc_n), 256, 0, s>>>(h->pc, dp, lines);
+  double *top = dst + h->nC - h->pc_n;
+  k_axpby2<double><<<grid_for(h->pc_n), 256, 0, s>>>(1.0, top, 1.0, h->pc, top, h->pc_n);
+  h->launches += 5;
+  MG_CUDA(cudaGetLastError());
+  return MF_OK;
+}

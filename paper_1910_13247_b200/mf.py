@@ -72,7 +72,8 @@ EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_
            "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing",
            "mf_partition", "mf_mg_create", "mf_mg_destroy", "mf_mg_levels", "mf_mg_level_size", "mf_mg_level_op",
            "mf_mg_level_lambda", "mf_mg_prolongate", "mf_mg_restrict", "mf_mg_vcycle", "mf_mg_cg_solve",
-           "mf_mg_set_stream", "mf_apply_f32", "mf_create_dg"]
+           "mf_mg_set_stream", "mf_apply_f32", "mf_create_dg", "mf_hng_create", "mf_hng_destroy", "mf_hng_sizes",
+           "mf_hng_apply", "mf_hng_set_stream"]
 
 _lib = None
 
@@ -122,6 +123,11 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "mf_mg_set_stream": [vp, vp],
         "mf_apply_f32": [vp, vp, i64, vp, i64],
         "mf_create_dg": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.POINTER(Coeff), ctypes.POINTER(vp)],
+        "mf_hng_create": [dp, dp, ctypes.c_double, i64p, i64, ctypes.c_int32, ctypes.POINTER(Coeff),
+                          ctypes.POINTER(vp)],
+        "mf_hng_sizes": [vp, i64p, i64p],
+        "mf_hng_apply": [vp, vp, i64, vp, i64],
+        "mf_hng_set_stream": [vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -131,6 +137,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.mf_destroy.restype = None
     L.mf_mg_destroy.argtypes = [vp]
     L.mf_mg_destroy.restype = None
+    L.mf_hng_destroy.argtypes = [vp]
+    L.mf_hng_destroy.restype = None
     L.mf_last_error.argtypes = []
     L.mf_last_error.restype = ctypes.c_char_p
     _lib = L
@@ -437,3 +445,49 @@ class Multigrid:
                                      self.n_local, rel_tol, max_iter, ctypes.byref(r),
                                      hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), history_cap))
         return x, CGResult(r.iterations, r.final_rel_residual, r.lambda_max, hist[:r.iterations].copy())
+
+
+class HangingNodeOperator:
+    """Q_k Laplacian on the two-block mesh with one 2:1 interface at z = z_mid
+    (include/mf.h, mf_hng_*): a coarse lower brick of n_cells_coarse cells and an upper
+    brick refined once more, hanging interface nodes eliminated by interpolation."""
+
+    def __init__(self, n_cells_coarse, nz_fine, degree, lower=(0.0, 0.0, 0.0), upper=(1.0, 1.0, 1.0), z_mid=0.5,
+                 coeff=1.0):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1910_13247_b200 needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        c = Coeff()
+        c.kind, c.value = 0, float(coeff)
+        lo = (ctypes.c_double * 3)(*lower)
+        hi = (ctypes.c_double * 3)(*upper)
+        nc = (ctypes.c_int64 * 3)(*n_cells_coarse)
+        h = ctypes.c_void_p()
+        L = load()
+        _check(L.mf_hng_create(lo, hi, z_mid, nc, nz_fine, degree, ctypes.byref(c), ctypes.byref(h)))
+        self._h = h
+        n, nC = ctypes.c_int64(), ctypes.c_int64()
+        _check(L.mf_hng_sizes(h, ctypes.byref(n), ctypes.byref(nC)))
+        self.n_local, self.n_coarse = n.value, nC.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().mf_hng_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def apply(self, src, dst=None):
+        t = self._torch
+        dst = t.zeros(self.n_local, dtype=t.float64, device=self.device) if dst is None else dst
+        for x, name in ((src, "src"), (dst, "dst")):
+            if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float64 and x.is_contiguous()
+                    and x.numel() == self.n_local):
+                raise TypeError(f"{name} must be a contiguous float64 CUDA tensor of {self.n_local} entries")
+        _check(load().mf_hng_set_stream(self._h, ctypes.c_void_p(t.cuda.current_stream(self.device).cuda_stream)))
+        _check(load().mf_hng_apply(self._h, ctypes.c_void_p(src.data_ptr()), self.n_local,
+                                   ctypes.c_void_p(dst.data_ptr()), self.n_local))
+        return dst
