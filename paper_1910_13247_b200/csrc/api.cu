@@ -38,6 +38,9 @@ struct mf_op {
   // planes on comm_stream while the interior layers run on stream
   bool zsplit = false;  // world > 1, or MF_ZSPLIT=1 (the same launch sequence on one GPU)
   bool dg = false;      // discontinuous (SIP) discretization, mf_create_dg
+  // pipelined mf_apply_host: copy-in / copy-out streams and per-range events
+  cudaStream_t h2d_s = nullptr, d2h_s = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   // live kernel timing (mf_set_kernel_timing)
@@ -248,6 +251,10 @@ extern "C" void mf_destroy(mf_op *op) {
   if (op->host_scal) cudaFreeHost(op->host_scal);
   for (cudaEvent_t e : op->ev) cudaEventDestroy(e);
   if (op->comm) ncclCommDestroy(op->comm);
+  for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : op->ev_out) cudaEventDestroy(e);
+  if (op->h2d_s) cudaStreamDestroy(op->h2d_s);
+  if (op->d2h_s) cudaStreamDestroy(op->d2h_s);
   if (op->ev_bnd) cudaEventDestroy(op->ev_bnd);
   if (op->ev_halo) cudaEventDestroy(op->ev_halo);
   if (op->comm_stream) cudaStreamDestroy(op->comm_stream);
@@ -439,9 +446,61 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
     CUDA_TRY(cudaMalloc(&op->h_src, bytes));
     CUDA_TRY(cudaMalloc(&op->h_dst, bytes));
   }
-  CUDA_TRY(cudaMemcpyAsync(op->h_src, src_host, bytes, cudaMemcpyHostToDevice, op->stream));
-  STATUS_TRY(apply_impl(op, op->h_src, op->h_dst));
-  CUDA_TRY(cudaMemcpyAsync(dst_host, op->h_dst, bytes, cudaMemcpyDeviceToHost, op->stream));
+  const Geo &g = op->g;
+  const char *pe = std::getenv("MF_HOST_PIPELINE");
+  const int C = (pe && std::atoi(pe) > 0) ? std::atoi(pe) : 8;
+  const int var = chosen_variant(op);
+  const bool pipelined = !op->dg && op->world == 1 && g.dim == 3 &&
+                         (var == kVariantCartPlane || var == kVariantGeneral) && C > 1 && g.nc[2] >= 2 * C;
+  if (!pipelined) {
+    CUDA_TRY(cudaMemcpyAsync(op->h_src, src_host, bytes, cudaMemcpyHostToDevice, op->stream));
+    STATUS_TRY(apply_impl(op, op->h_src, op->h_dst));
+    CUDA_TRY(cudaMemcpyAsync(dst_host, op->h_dst, bytes, cudaMemcpyDeviceToHost, op->stream));
+    CUDA_TRY(cudaStreamSynchronize(op->stream));
+    return MF_OK;
+  }
+  // Pipelined: the cell layers in C z-ranges; range r's input planes go up on h2d_s, its
+  // apply (init / zeroing + kernel for those layers) runs on the op's stream once they are in,
+  // and its finished output planes come down on d2h_s while range r+1 is copied in and
+  // computed -- host->device and device->host transfers overlap (full duplex).
+  if (!op->h2d_s) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&op->h2d_s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&op->d2h_s, cudaStreamNonBlocking));
+  }
+  while ((int)op->ev_in.size() < C) {
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    op->ev_in.push_back(a);
+    op->ev_out.push_back(b);
+  }
+  const int64_t K = g.k, nz = g.nc[2], pl = op->plane;
+  // the previous call's work on the op's stream is done before its buffers are reused
+  CUDA_TRY(cudaEventRecord(op->ev_out[C - 1], op->stream));
+  CUDA_TRY(cudaStreamWaitEvent(op->h2d_s, op->ev_out[C - 1], 0));
+  for (int r = 0; r < C; ++r) {
+    const int64_t z0 = nz * r / C, z1 = nz * (r + 1) / C;
+    const int64_t in0 = r == 0 ? 0 : K * z0 + 1, in1 = K * z1;  // node planes, inclusive
+    CUDA_TRY(cudaMemcpyAsync(op->h_src + in0 * pl, src_host + in0 * pl, (in1 - in0 + 1) * pl * sizeof(double),
+                             cudaMemcpyHostToDevice, op->h2d_s));
+    CUDA_TRY(cudaEventRecord(op->ev_in[r], op->h2d_s));
+    CUDA_TRY(cudaStreamWaitEvent(op->stream, op->ev_in[r], 0));
+    if (var == kVariantCartPlane) {
+      CUDA_TRY(launch_apply_cart_plane_range(g, op->t, op->h_src, op->h_dst, op->stream, &op->launches, (int)z0,
+                                             (int)z1));
+    } else {  // zero the planes no earlier range has touched, then add this range's cells
+      CUDA_TRY(launch_zero(op->h_dst + in0 * pl, (in1 - in0 + 1) * pl, op->stream, &op->launches));
+      const int64_t layer = g.nc[0] * g.nc[1];
+      CUDA_TRY(launch_apply_general_cells(g, op->t, op->h_src, op->h_dst, op->metric, op->stream, &op->launches,
+                                          z0 * layer, z1 * layer));
+    }
+    CUDA_TRY(cudaEventRecord(op->ev_out[r], op->stream));
+    const int64_t out0 = K * z0, out1 = r == C - 1 ? K * z1 : K * z1 - 1;  // finished planes
+    CUDA_TRY(cudaStreamWaitEvent(op->d2h_s, op->ev_out[r], 0));
+    CUDA_TRY(cudaMemcpyAsync(dst_host + out0 * pl, op->h_dst + out0 * pl, (out1 - out0 + 1) * pl * sizeof(double),
+                             cudaMemcpyDeviceToHost, op->d2h_s));
+  }
+  CUDA_TRY(cudaStreamSynchronize(op->d2h_s));
   CUDA_TRY(cudaStreamSynchronize(op->stream));
   return MF_OK;
 }

@@ -77,6 +77,13 @@ cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double 
 // instantiated for float (dst zeroed by the caller for the general kernel)
 cudaError_t launch_apply_cart_plane_f32(const Geo &g, const Tables &t, const float *src, float *dst,
                                         cudaStream_t s, int64_t *launches);
+// the cell layers [zr_lo, zr_hi) only, with their share of dst initialisation (the
+// pipelined host apply: ranges launched in increasing z complete the apply)
+cudaError_t launch_apply_cart_plane_range(const Geo &g, const Tables &t, const double *src, double *dst,
+                                          cudaStream_t s, int64_t *launches, int zr_lo, int zr_hi);
+cudaError_t launch_apply_general_cells(const Geo &g, const Tables &t, const double *src, double *dst,
+                                       const double *metric, cudaStream_t s, int64_t *launches, int64_t cb,
+                                       int64_t ce);
 cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float *src, float *dst,
                                      const float *metric, cudaStream_t s, int64_t *launches);
 bool cart_plane_supported(const Geo &g);

@@ -908,6 +908,13 @@ static cudaError_t general_range(const Geo &g, const Tables &t, const double *sr
   return dispatch_k<3, 2>(g, t, src, dst, metric, s, cb, ce);
 }
 
+// cells [cb, ce) only (the caller zeroes their dst planes not touched by earlier ranges)
+cudaError_t launch_apply_general_cells(const Geo &g, const Tables &t, const double *src, double *dst,
+                                       const double *metric, cudaStream_t s, int64_t *launches, int64_t cb,
+                                       int64_t ce) {
+  return general_range(g, t, src, dst, metric, s, launches, cb, ce);
+}
+
 // (the caller zeroes dst before part 0 / part 1)
 cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
                                  const double *metric, cudaStream_t s, int64_t *launches, int part) {

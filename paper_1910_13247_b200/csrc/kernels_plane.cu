@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
         prefetch(item_of(next), item_of(next).cz_begin, 0);
       }
       const uint32_t zm = ((z_lo_c && cz == 0) ? 1u : 0u) | ((z_hi_c && cz == P.ncz - 1) ? 1u << K : 0u);
-      const uint32_t am = ((first && chunk > 0) ? 1u : 0u) | ((last && chunk < P.nch - 1) ? 1u << K : 0u);
+      const uint32_t am = ((first && (chunk > 0 || P.lo_shared)) ? 1u : 0u) |
+                          ((last && (chunk < P.nch - 1 || P.hi_shared)) ? 1u << K : 0u);
       T *outl = dst + base0 + (int64_t)K * (cz - cz_begin) * plane;
       if (own_ok) {
 #pragma unroll
@@ -354,9 +355,10 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
 
 // part 0: init + every chunk; part 1: init + the two boundary chunks of the z-split;
 // part 2: the interior chunks of the z-split (see TileParams::zsplit)
+// part 3: init + the cell layers [zr_lo, zr_hi) only (the pipelined host apply)
 template <int K, int TX, int TY, bool ISO, class T>
 static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T *dst, cudaStream_t s,
-                                  int64_t *launches, int part) {
+                                  int64_t *launches, int part, int zr_lo = 0, int zr_hi = 0) {
   using S = PlaneShape<K, TX, TY>;
   TileParams P;
   tile_params_common(g, t, TX, TY, &P);
@@ -373,8 +375,21 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T
   }
   const int slots = sms * occ;
   // the bottom plane costs one extra face per cell
-  if (part == 0) tile_choose_chunks(&P, slots, 1.0 / K + 0.25);
-  else tile_choose_chunks_split(&P, slots, 1.0 / K + 0.25);
+  if (part == 0) {
+    tile_choose_chunks(&P, slots, 1.0 / K + 0.25);
+  } else if (part == 3) {
+    TileParams Q = P;
+    Q.ncz = zr_hi - zr_lo;
+    tile_choose_chunks(&Q, slots, 1.0 / K + 0.25);
+    P.LZ = Q.LZ;
+    P.nch = Q.nch;
+    P.zr_lo = zr_lo;
+    P.zr_hi = zr_hi;
+    P.lo_shared = zr_lo > 0;
+    P.hi_shared = zr_hi < P.ncz;
+  } else {
+    tile_choose_chunks_split(&P, slots, 1.0 / K + 0.25);
+  }
   P.pass = part;
   if (part != 2) {
     cudaError_t e = tile_launch_init(P, g, K, TX, TY, src, dst, s, launches);
@@ -392,11 +407,11 @@ bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }
 
 template <class T>
 static cudaError_t launch_cart_plane_any(const Geo &g, const Tables &t, const T *src, T *dst, cudaStream_t s,
-                                        int64_t *launches, int part) {
+                                        int64_t *launches, int part, int zr_lo = 0, int zr_hi = 0) {
   const bool iso = g.fcart[0] == g.fcart[1] && g.fcart[0] == g.fcart[2];
-#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                                    \
-  return iso ? launch_plane_t<KK, TXX, TYY, true, T>(g, t, src, dst, s, launches, part)  \
-             : launch_plane_t<KK, TXX, TYY, false, T>(g, t, src, dst, s, launches, part)
+#define MF_PLANE_LAUNCH(KK, TXX, TYY)                                                                   \
+  return iso ? launch_plane_t<KK, TXX, TYY, true, T>(g, t, src, dst, s, launches, part, zr_lo, zr_hi)  \
+             : launch_plane_t<KK, TXX, TYY, false, T>(g, t, src, dst, s, launches, part, zr_lo, zr_hi)
   switch (g.k) {
     case 2: MF_PLANE_LAUNCH(2, 8, 8);
     case 3: MF_PLANE_LAUNCH(3, 8, 4);
@@ -414,6 +429,11 @@ cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double 
 cudaError_t launch_apply_cart_plane_f32(const Geo &g, const Tables &t, const float *src, float *dst, cudaStream_t s,
                                         int64_t *launches) {
   return launch_cart_plane_any<float>(g, t, src, dst, s, launches, 0);
+}
+
+cudaError_t launch_apply_cart_plane_range(const Geo &g, const Tables &t, const double *src, double *dst,
+                                          cudaStream_t s, int64_t *launches, int zr_lo, int zr_hi) {
+  return launch_cart_plane_any<double>(g, t, src, dst, s, launches, 3, zr_lo, zr_hi);
 }
 
 }  // namespace mf

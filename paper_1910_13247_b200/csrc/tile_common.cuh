@@ -37,6 +37,9 @@ struct TileParams {
   // interior layers in chunks of LZ; pass 1 = the two boundary chunks, pass 2 = the rest
   // (pass 0 = every chunk).  Without zsplit chunk c = layers [c LZ, (c+1) LZ).
   int zsplit, pass;
+  // pass 3 (layer range, the pipelined host apply): only cell layers [zr_lo, zr_hi), in
+  // chunks of LZ; planes shared with the neighbouring ranges take atomics
+  int zr_lo, zr_hi, lo_shared, hi_shared;
   uint32_t dirichlet;
   int skip_top_identity;
   unsigned long long *prof;  // debug counters [2][8] or null
@@ -125,6 +128,7 @@ struct PlaneSet {
   int64_t c0[12], stride[12], lines[12];  // lines = count x lines per plane
   int64_t total_lines;
   int nfam;
+  int gz_lo, gz_hi;  // the node planes the x- and y-plane families cover (a layer range)
 };
 
 template <class T>
@@ -142,8 +146,8 @@ static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant_
     int64_t l = L;
     while (f < ps.nfam - 1 && l >= ps.lines[f]) l -= ps.lines[f++];
     const int axis = ps.axis[f];
-    const int nlines = axis == 2 ? Ny : Nz, nnodes = axis == 0 ? Ny : Nx;
-    const int pl = (int)(l / nlines), line = (int)(l - (int64_t)pl * nlines);
+    const int nlines = axis == 2 ? Ny : ps.gz_hi - ps.gz_lo + 1, nnodes = axis == 0 ? Ny : Nx;
+    const int pl = (int)(l / nlines), line = (int)(l - (int64_t)pl * nlines) + (axis == 2 ? 0 : ps.gz_lo);
     const int c = (int)(ps.c0[f] + ps.stride[f] * pl);
     if (sizeof(T) == 8 && axis == 0 && c >= 4 && c + 4 < Nx && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
       // strided x-plane nodes: write the whole aligned 32-byte sector around each
@@ -313,17 +317,20 @@ static inline void tile_choose_chunks_split(TileParams *P, int slots, double per
 
 // items (tile, chunk) of a pass, and the chunk's cell layers
 __host__ __device__ inline int tile_pass_chunks(const TileParams &P) {
-  if (P.pass == 0) return P.nch;
+  if (P.pass == 0 || P.pass == 3) return P.nch;
   if (P.pass == 1) return P.nch >= 2 ? 2 : 1;
   return P.nch > 2 ? P.nch - 2 : 0;
 }
 __host__ __device__ inline int tile_pass_chunk(const TileParams &P, int j) {
-  if (P.pass == 0) return j;
+  if (P.pass == 0 || P.pass == 3) return j;
   if (P.pass == 1) return j == 0 ? 0 : P.nch - 1;
   return 1 + j;
 }
 __host__ __device__ inline void tile_chunk_layers(const TileParams &P, int c, int &b, int &e) {
-  if (!P.zsplit) {
+  if (P.pass == 3) {
+    b = P.zr_lo + c * P.LZ;
+    e = b + P.LZ < P.zr_hi ? b + P.LZ : P.zr_hi;
+  } else if (!P.zsplit) {
     b = c * P.LZ;
     e = b + P.LZ < P.ncz ? b + P.LZ : P.ncz;
   } else if (c == 0) {
@@ -345,6 +352,12 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
                                            const T *src, T *dst, cudaStream_t s, int64_t *launches) {
   PlaneSet ps;
   std::memset(&ps, 0, sizeof(ps));
+  // the node planes this launch owns: all, or for a layer range (pass 3) the planes of
+  // its layers except the bottom one when the range below already initialised it
+  const bool range = P.pass == 3;
+  ps.gz_lo = range ? K * P.zr_lo + (P.lo_shared ? 1 : 0) : 0;
+  ps.gz_hi = range ? K * P.zr_hi : (int)P.Nz - 1;
+  const int nzl = ps.gz_hi - ps.gz_lo + 1;
   int total = 0;
   auto fam = [&](int axis, int64_t c0, int64_t stride, int count) {
     if (count <= 0) return;
@@ -352,12 +365,15 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
     ps.c0[ps.nfam] = c0;
     ps.stride[ps.nfam] = stride;
     ps.count[ps.nfam] = count;
-    ps.lines[ps.nfam++] = (int64_t)count * (axis == 2 ? P.Ny : P.Nz);
+    ps.lines[ps.nfam++] = (int64_t)count * (axis == 2 ? P.Ny : nzl);
     total += count;
   };
   fam(0, (int64_t)K * TX, (int64_t)K * TX, P.ntx - 1);
   fam(1, (int64_t)K * TY, (int64_t)K * TY, P.nty - 1);
-  if (!P.zsplit) {
+  if (range) {  // chunk planes inside the range, and its top plane if a range above shares it
+    fam(2, (int64_t)K * (P.zr_lo + P.LZ), (int64_t)K * P.LZ, P.nch - 1);
+    if (P.hi_shared) fam(2, (int64_t)K * P.zr_hi, 1, 1);
+  } else if (!P.zsplit) {
     fam(2, (int64_t)K * P.LZ, (int64_t)K * P.LZ, P.nch - 1);
   } else if (P.nch >= 2) {  // bottom planes of chunks 1 .. nch-1
     fam(2, (int64_t)K, (int64_t)K * P.LZ, P.nch - 2);
@@ -367,8 +383,8 @@ static inline cudaError_t tile_launch_init(const TileParams &P, const Geo &g, in
   if (g.dirichlet & 2u) fam(0, P.Nx - 1, 1, 1);
   if (g.dirichlet & 4u) fam(1, 0, 1, 1);
   if (g.dirichlet & 8u) fam(1, P.Ny - 1, 1, 1);
-  if (g.dirichlet & 16u) fam(2, 0, 1, 1);
-  if ((g.dirichlet & 32u) || g.skip_top_identity) fam(2, P.Nz - 1, 1, 1);
+  if ((g.dirichlet & 16u) && (!range || P.zr_lo == 0)) fam(2, 0, 1, 1);
+  if (((g.dirichlet & 32u) || g.skip_top_identity) && (!range || P.zr_hi == P.ncz)) fam(2, P.Nz - 1, 1, 1);
   if (total == 0) return cudaSuccess;
   ++*launches;
   for (int f = 0; f < ps.nfam; ++f) ps.total_lines += ps.lines[f];

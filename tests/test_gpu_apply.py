@@ -181,6 +181,40 @@ def test_apply_host_matches_device(torch):
     assert rel_l2(y_host, y_dev) < 1e-15
 
 
+HOST_PIPELINE_CASES = [
+    (dict(dim=3, n_cells=(9, 10, 11), k=2), "4", "plane"),                # ragged ranges (3,3,3,2 layers)
+    (dict(dim=3, n_cells=(6, 5, 16), k=4), "4", "plane"),
+    (dict(dim=3, n_cells=(6, 5, 16), k=4, dirichlet=0), "3", "plane"),
+    (dict(dim=3, n_cells=(9, 17, 13), k=3, dirichlet=0b011001), "5", "plane"),
+    (dict(dim=3, n_cells=(5, 3, 20), k=4, dirichlet=0b110000), "2", "plane"),
+    (dict(dim=3, n_cells=(4, 4, 8), k=3), "4", "plane"),                   # two layers per range
+    (dict(dim=3, n_cells=(4, 4, 16), k=3), "8", "plane"),
+    (dict(dim=3, n_cells=(5, 4, 11), k=3, geometry="sine", coeff="variable"), "4", "auto"),
+    (dict(dim=3, n_cells=(3, 4, 9), k=5, dirichlet=0b100110), "3", "auto"),
+    (dict(dim=3, n_cells=(6, 5, 8), k=2, coeff="variable", dirichlet=0), "4", "general"),
+    (dict(dim=3, n_cells=(6, 5, 16), k=4), "8", "general"),
+]
+
+
+@pytest.mark.parametrize("case,chunks,variant", HOST_PIPELINE_CASES,
+                         ids=lambda v: v if isinstance(v, str) else _id(v))
+def test_pipelined_apply_host_matches_oracle(case, chunks, variant, torch, monkeypatch):
+    # mf_apply_host overlaps the copies with the apply by z cell-layer ranges
+    monkeypatch.setenv("MF_HOST_PIPELINE", chunks)
+    p = oracle_problem(case)
+    A = oracle.CSR(p)
+    op = cuda_operator(case)
+    op.set_variant(variant)
+    for s in (1, 2, 3):
+        x = seeded(A.n, s)
+        y = op.apply_host(x)
+        assert rel_l2(y, A @ x) <= CUDA_ORACLE_TOL, (s, rel_l2(y, A @ x))
+        y_dev = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_l2(y, y_dev) <= 1e-14
+    m = oracle.constrained_mask_fast(p)
+    np.testing.assert_array_equal(y[m], x[m])
+
+
 def test_length_and_argument_errors(torch):
     from paper_1910_13247_b200 import MFError
 
