@@ -98,6 +98,53 @@ const char *mf_last_error(void);
  * mf_get_info reports apply_variant 4). */
 mf_status mf_create_dg(const mf_mesh *mesh, int32_t degree, const mf_coeff *coeff, mf_op **out);
 
+/* General unstructured hexahedral mesh (§3.1
+ * "unstructured ... hexahedral meshes", §3.5 hanging-node constraints applied
+ * inside the matrix-free loop; R21, R22).  All arrays are HOST memory, read
+ * during mf_create_hex only (copied to the device; the caller keeps ownership).
+ *   vertices       [n_vertices][3] fp64 coordinates
+ *   cell_vertices  [n_cells][8] int32: the cell's vertices in its own lexicographic frame
+ *                  (local vertex a + 2b + 4c at reference corner (a,b,c)); the mapping is
+ *                  trilinear (R21) and must have det J > 0 at every Gauss point
+ *                  (else MF_ERR_SINGULAR)
+ *   cell_dofs      [n_cells][(k+1)^3] int32, local GLL node i = i0 + (k+1)(i1 + (k+1) i2):
+ *                  >= 0 the global DoF (< n_dofs); < 0 constraint line -1 - value (R22)
+ *   line_ptr       [n_lines+1] int32 CSR offsets into line_dof / line_w; a constrained
+ *                  (hanging) local node takes u = sum line_w[j] u[line_dof[j]] in the gather
+ *                  and receives the transpose in the scatter (may be NULL if n_lines == 0)
+ *   dirichlet_dofs [n_dirichlet] int32: identity rows / columns (R3); gather reads them as
+ *                  zero, line entries on them drop out
+ * mf_hex_number_dofs builds cell_dofs for a conforming mesh.  The returned op works with
+ * mf_apply, mf_apply_host, mf_diagonal, mf_estimate_lambda_max, mf_chebyshev and
+ * mf_cg_solve (one rank; mf_get_info reports apply_variant 5, n_local = n_dofs).
+ * Errors: MF_ERR_ARGUMENT for null arrays, indices out of range, degree outside 1..8. */
+typedef struct {
+  int64_t n_vertices, n_cells, n_dofs, n_lines, n_dirichlet;
+  const double *vertices;
+  const int32_t *cell_vertices;
+  const int32_t *cell_dofs;
+  const int32_t *line_ptr;
+  const int32_t *line_dof;
+  const double *line_w;
+  const int32_t *dirichlet_dofs;
+} mf_hex_mesh;
+mf_status mf_create_hex(const mf_hex_mesh *mesh, int32_t degree, const mf_coeff *coeff, mf_op **out);
+
+/* DoF numbering of a conforming hex mesh (host only; the DoF handler step of
+ * P:694-705): one DoF per vertex, k-1 per edge, (k-1)^2 per face, (k-1)^3 per cell
+ * interior, numbered in order of first appearance cell by cell.  Edge and face DoFs
+ * are laid out in a frame fixed by the GLOBAL vertex numbers (an edge runs from its
+ * smaller to its larger vertex; a face's origin is its smallest vertex, its first axis
+ * points to the smaller of the origin's two face neighbours), so cells that see a
+ * shared edge or face in different orientations agree on its DoFs (R21).
+ *   cell_vertices [n_cells][8] as for mf_hex_mesh; cell_dofs [n_cells][(k+1)^3] output;
+ *   *n_dofs output.  is_boundary (optional, may be NULL) [capacity] uint8 output: 1 on the
+ *   DoFs of faces that belong to one cell only; MF_ERR_LENGTH if n_dofs > capacity.
+ * Errors: MF_ERR_ARGUMENT for a cell with repeated vertices or a face shared by more
+ * than two cells (non-manifold / non-conforming input). */
+mf_status mf_hex_number_dofs(int32_t degree, int64_t n_cells, const int32_t *cell_vertices, int32_t *cell_dofs,
+                             int64_t *n_dofs, uint8_t *is_boundary, int64_t capacity);
+
 /* NCCL unique id (128 bytes) for mf_dist, created on rank 0 and broadcast by the caller. */
 mf_status mf_nccl_unique_id(uint8_t *out128);
 

@@ -2,6 +2,6 @@
 
 The product is libmf_b200.so (C ABI in include/mf.h, CUDA sm_100a kernels);
 this package is its thin ctypes binding.  See DESIGN.md."""
-from .mf import HangingNodeOperator, MFError, Multigrid, Operator, load  # noqa: F401
+from .mf import HangingNodeOperator, HexOperator, MFError, Multigrid, Operator, hex_number_dofs, load  # noqa: F401
 
-__all__ = ["Operator", "Multigrid", "HangingNodeOperator", "MFError", "load"]
+__all__ = ["Operator", "Multigrid", "HangingNodeOperator", "HexOperator", "hex_number_dofs", "MFError", "load"]

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <climits>
 #include <functional>
 #include <cmath>
 #include <cstdio>
@@ -38,6 +39,8 @@ struct mf_op {
   // planes on comm_stream while the interior layers run on stream
   bool zsplit = false;  // world > 1, or MF_ZSPLIT=1 (the same launch sequence on one GPU)
   bool dg = false;      // discontinuous (SIP) discretization, mf_create_dg
+  bool hex = false;     // unstructured hex mesh, mf_create_hex (device arrays in hx)
+  HexDev hx{};
   // pipelined mf_apply_host: copy-in / copy-out streams and per-range events
   cudaStream_t h2d_s = nullptr, d2h_s = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
@@ -248,6 +251,12 @@ extern "C" void mf_destroy(mf_op *op) {
   for (double *b : {op->diag, op->dinv, op->r, op->p, op->v, op->z, op->cd, op->cax, op->partials, op->dev_scal,
                     op->h_src, op->h_dst, op->recv_lo, op->recv_hi})
     cudaFree(b);
+  cudaFree((void *)op->hx.cell_dofs);
+  cudaFree((void *)op->hx.line_ptr);
+  cudaFree((void *)op->hx.line_dof);
+  cudaFree((void *)op->hx.line_w);
+  cudaFree((void *)op->hx.cell_lines);
+  cudaFree((void *)op->hx.dir);
   if (op->host_scal) cudaFreeHost(op->host_scal);
   for (cudaEvent_t e : op->ev) cudaEventDestroy(e);
   if (op->comm) ncclCommDestroy(op->comm);
@@ -279,6 +288,141 @@ extern "C" mf_status mf_create_dg(const mf_mesh *mesh, int32_t degree, const mf_
   return MF_OK;
 }
 
+// Unstructured hex mesh: cell_dofs / constraint lines / Dirichlet list
+// checked and copied to the device, the trilinear metric computed once
+extern "C" mf_status mf_create_hex(const mf_hex_mesh *m, int32_t degree, const mf_coeff *coeff, mf_op **out) {
+  if (!m || !coeff || !out) return fail(MF_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (degree < 1 || degree > 8) return fail(MF_ERR_ARGUMENT, "degree must be in 1..8");
+  if (coeff->kind != MF_COEFF_CONSTANT && coeff->kind != MF_COEFF_VARIABLE)
+    return fail(MF_ERR_ARGUMENT, "unknown coefficient kind");
+  if (coeff->kind == MF_COEFF_CONSTANT && !(coeff->value > 0.0))
+    return fail(MF_ERR_ARGUMENT, "constant coefficient must be > 0");
+  if (m->n_cells < 0 || m->n_vertices < 1 || m->n_dofs < 1 || m->n_dofs > INT32_MAX || m->n_lines < 0 ||
+      m->n_dirichlet < 0)
+    return fail(MF_ERR_ARGUMENT, "bad sizes");
+  if (!m->vertices || !m->cell_vertices || !m->cell_dofs || (m->n_lines > 0 && (!m->line_ptr || !m->line_dof ||
+                                                                                !m->line_w)) ||
+      (m->n_dirichlet > 0 && !m->dirichlet_dofs))
+    return fail(MF_ERR_ARGUMENT, "null array");
+  const int64_t NV = ipow(degree + 1, 3), nc = m->n_cells, nd = m->n_dofs;
+  for (int64_t i = 0; i < 8 * nc; ++i)
+    if (m->cell_vertices[i] < 0 || m->cell_vertices[i] >= m->n_vertices)
+      return fail(MF_ERR_ARGUMENT, "cell_vertices entry out of range");
+  std::vector<uint8_t> is_dir(nd, 0);
+  for (int64_t i = 0; i < m->n_dirichlet; ++i) {
+    const int32_t d = m->dirichlet_dofs[i];
+    if (d < 0 || d >= nd) return fail(MF_ERR_ARGUMENT, "dirichlet_dofs entry out of range");
+    is_dir[d] = 1;
+  }
+  std::vector<int32_t> dir;
+  for (int64_t d = 0; d < nd; ++d)
+    if (is_dir[d]) dir.push_back((int32_t)d);
+  // constraint lines without their Dirichlet entries (those values are zero)
+  std::vector<int32_t> lp(1, 0), ld;
+  std::vector<double> lw;
+  if (m->n_lines > 0 && (m->line_ptr[0] != 0)) return fail(MF_ERR_ARGUMENT, "line_ptr[0] != 0");
+  for (int64_t l = 0; l < m->n_lines; ++l) {
+    if (m->line_ptr[l + 1] < m->line_ptr[l]) return fail(MF_ERR_ARGUMENT, "line_ptr not monotone");
+    for (int32_t j = m->line_ptr[l]; j < m->line_ptr[l + 1]; ++j) {
+      const int32_t d = m->line_dof[j];
+      if (d < 0 || d >= nd) return fail(MF_ERR_ARGUMENT, "line_dof entry out of range");
+      if (is_dir[d]) continue;
+      ld.push_back(d);
+      lw.push_back(m->line_w[j]);
+    }
+    lp.push_back((int32_t)ld.size());
+  }
+  std::vector<int32_t> cd(m->cell_dofs, m->cell_dofs + nc * NV);
+  std::vector<uint8_t> cl(nc, 0);
+  for (int64_t c = 0; c < nc; ++c)
+    for (int64_t i = 0; i < NV; ++i) {
+      int32_t &d = cd[c * NV + i];
+      if (d >= 0) {
+        if (d >= nd) return fail(MF_ERR_ARGUMENT, "cell_dofs entry >= n_dofs");
+        if (is_dir[d]) d = kHexDirichlet;
+      } else {
+        if (d == kHexDirichlet || -1 - (int64_t)d >= m->n_lines)
+          return fail(MF_ERR_ARGUMENT, "cell_dofs refers to a missing constraint line");
+        cl[c] = 1;
+      }
+    }
+  int device = 0;
+  CUDA_TRY(cudaGetDevice(&device));
+  mf_op *op = new mf_op();
+  op->device = device;
+  op->hex = true;
+  Geo &g = op->g;
+  std::memset(&g, 0, sizeof(Geo));
+  g.dim = 3;
+  g.k = degree;
+  g.nc[0] = nc;
+  g.nc[1] = g.nc[2] = 1;
+  g.geom = MF_GEOM_SINE;  // a stored metric (reported as curved geometry)
+  g.coeff_kind = coeff->kind;
+  g.coeff = coeff->value;
+  build_tables(degree, &op->t);
+  op->n_local = op->n_global = op->n_owned = nd;
+  auto cleanup = [&](mf_status st) {
+    mf_destroy(op);
+    return st;
+  };
+  auto upload = [&](const void *h, size_t bytes, void **d) -> bool {
+    if (bytes == 0) bytes = 8;  // a valid pointer for empty arrays
+    if (cudaMalloc(d, bytes) != cudaSuccess) return false;
+    return h == nullptr || cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  HexDev &h = op->hx;
+  h.ncells = nc;
+  h.ndofs = nd;
+  h.ndir = (int64_t)dir.size();
+  void *p_cd, *p_lp, *p_ld, *p_lw, *p_cl, *p_dir, *p_v = nullptr, *p_cv = nullptr;
+  bool ok = upload(cd.data(), cd.size() * 4, &p_cd) && upload(lp.data(), lp.size() * 4, &p_lp) &&
+            upload(ld.empty() ? nullptr : ld.data(), ld.size() * 4, &p_ld) &&
+            upload(lw.empty() ? nullptr : lw.data(), lw.size() * 8, &p_lw) && upload(cl.data(), cl.size(), &p_cl) &&
+            upload(dir.empty() ? nullptr : dir.data(), dir.size() * 4, &p_dir);
+  h.cell_dofs = (const int32_t *)p_cd;
+  h.line_ptr = (const int32_t *)p_lp;
+  h.line_dof = (const int32_t *)p_ld;
+  h.line_w = (const double *)p_lw;
+  h.cell_lines = (const uint8_t *)p_cl;
+  h.dir = (const int32_t *)p_dir;
+  if (!ok) return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "hex mesh arrays"));
+  if (cudaMallocHost(&op->host_scal, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->dev_scal, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->partials, 3 * kDotBlocks * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->metric, 6 * nc * NV * sizeof(double) + 8) != cudaSuccess)
+    return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "scalar / metric buffers"));
+  h.metric = op->metric;
+  int *bad = nullptr;
+  ok = upload(m->vertices, m->n_vertices * 3 * sizeof(double), &p_v) &&
+       upload(m->cell_vertices, nc * 8 * sizeof(int32_t), &p_cv) && cudaMalloc(&bad, sizeof(int)) == cudaSuccess;
+  cudaError_t e = ok ? cudaMemset(bad, 0, sizeof(int)) : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess)
+    e = launch_hex_metric(degree, op->t, (const double *)p_v, (const int32_t *)p_cv, nc, coeff->kind, coeff->value,
+                          op->metric, bad, 0, &op->launches);
+  int hbad = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  cudaFree(p_v);
+  cudaFree(p_cv);
+  if (e != cudaSuccess) return cleanup(fail(MF_ERR_CUDA, std::string("hex metric: ") + cudaGetErrorString(e)));
+  if (hbad) return cleanup(fail(MF_ERR_SINGULAR, "det J <= 0 at a quadrature point"));
+  *out = op;
+  return MF_OK;
+}
+
+extern "C" mf_status mf_hex_number_dofs(int32_t degree, int64_t n_cells, const int32_t *cell_vertices,
+                                        int32_t *cell_dofs, int64_t *n_dofs, uint8_t *is_boundary,
+                                        int64_t capacity) {
+  if (!cell_vertices || !cell_dofs || !n_dofs) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (degree < 1 || degree > 8) return fail(MF_ERR_ARGUMENT, "degree must be in 1..8");
+  if (n_cells < 0) return fail(MF_ERR_ARGUMENT, "n_cells < 0");
+  std::string err;
+  mf_status st = hex_number_dofs(degree, n_cells, cell_vertices, cell_dofs, n_dofs, is_boundary, capacity, &err);
+  return st == MF_OK ? MF_OK : fail(st, err);
+}
+
 extern "C" mf_status mf_sizes(const mf_op *op, int64_t *n_local, int64_t *first_global, int64_t *n_global,
                               int64_t *n_owned) {
   if (!op) return fail(MF_ERR_ARGUMENT, "null op");
@@ -296,12 +440,15 @@ extern "C" mf_status mf_set_stream(mf_op *op, void *s) {
 }
 
 static int chosen_variant(const mf_op *op) {
+  if (op->hex) return kVariantHex;
+  if (op->dg) return kVariantDG;
   if (op->variant != kVariantAuto) return op->variant;
   return cart_plane_supported(op->g) ? kVariantCartPlane : kVariantGeneral;
 }
 
 extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
   if (!op) return fail(MF_ERR_ARGUMENT, "null op");
+  if (op->hex || op->dg) return fail(MF_ERR_ARGUMENT, "DG / hex operators have one kernel family");
   if ((variant == kVariantCartTile && !cart_tile_supported(op->g)) ||
       (variant == kVariantCartPlane && !cart_plane_supported(op->g)))
     return fail(MF_ERR_ARGUMENT, "tile/plane kernels need dim 3, Cartesian geometry, constant coefficient, k 2..4");
@@ -385,6 +532,12 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
 }
 
 static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
+  if (op->hex) {
+    CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
+    STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_apply_hex(op->g.k, op->t, op->hx, src, dst, op->stream, &op->launches));
+    return timing_mark(op);
+  }
   if (op->dg) {
     STATUS_TRY(timing_mark(op));
     CUDA_TRY(launch_apply_dg(op->g, op->t, src, dst, op->stream, &op->launches));
@@ -506,6 +659,11 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
 }
 
 static mf_status diagonal_impl(mf_op *op, double *diag) {
+  if (op->hex) {
+    CUDA_TRY(launch_zero(diag, op->n_local, op->stream, &op->launches));
+    CUDA_TRY(launch_diagonal_hex(op->g.k, op->t, op->hx, diag, op->stream, &op->launches));
+    return MF_OK;
+  }
   if (op->dg) {
     CUDA_TRY(launch_diagonal_dg(op->g, op->t, diag, op->stream, &op->launches));
     return MF_OK;
@@ -575,7 +733,8 @@ static mf_status lambda_impl(mf_op *op, int steps, double *lam) {
   cudaStream_t s = op->stream;
   double *r = op->r, *z = op->z, *p = op->p, *v = op->v;
   CUDA_TRY(launch_splitmix(r, n, op->first_global, 0, s, &op->launches));
-  if (!op->dg) CUDA_TRY(launch_set_constrained(op->g, r, 0.0, s, &op->launches));  // (DG: no constrained DoFs)
+  if (op->hex) CUDA_TRY(launch_hex_set(op->hx, r, 0.0, s, &op->launches));
+  else if (!op->dg) CUDA_TRY(launch_set_constrained(op->g, r, 0.0, s, &op->launches));  // (DG: no constrained DoFs)
   CUDA_TRY(launch_mul(op->dinv, r, z, n, s, &op->launches));
   CUDA_TRY(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   {
@@ -664,7 +823,8 @@ static mf_status ensure_f32(mf_op *op) {
 }
 
 mf_status apply_f32(mf_op *op, const float *src, float *dst) {
-  if (op->world != 1 || op->g.dim != 3 || op->dg) return fail(MF_ERR_ARGUMENT, "FP32 apply: 3D CG, one rank");
+  if (op->world != 1 || op->g.dim != 3 || op->dg || op->hex)
+    return fail(MF_ERR_ARGUMENT, "FP32 apply: 3D CG brick, one rank");
   STATUS_TRY(ensure_f32(op));
   if (chosen_variant(op) == kVariantCartPlane) {
     CUDA_TRY(launch_apply_cart_plane_f32(op->g, op->t, src, dst, op->stream, &op->launches));
@@ -798,10 +958,15 @@ extern "C" mf_status mf_get_info(const mf_op *op, mf_info *info) {
   info->degree = g.k;
   info->geometry = g.geom;
   info->coeff_kind = g.coeff_kind;
-  info->apply_variant = op->dg ? 4 : chosen_variant(op);
+  info->apply_variant = chosen_variant(op);
   info->n_cells_local = ncells_local(g);
   info->kernel_launches = op->launches;
   const int64_t nq = ipow(g.k + 1, g.dim);
+  if (op->hex) {  // src + dst, metric (6 doubles) and cell_dofs (int32) per cell node / point
+    info->bytes_algorithmic = 16 * op->n_local + (8 * 6 + 4) * op->hx.ncells * nq;
+    info->flops_algorithmic = (double)op->hx.ncells * (2.0 * 12.0 * std::pow(g.k + 1.0, 4) + 18.0 * nq);
+    return MF_OK;
+  }
   info->bytes_algorithmic =
       16 * op->n_local + (g.geom == MF_GEOM_SINE ? 8 * (int64_t)ncomp(g.dim) * ncells_local(g) * nq : 0);
   // 12-sweep (3D) / 8-sweep (2D) collocation kernel: 2 * (2 dim sweeps) * N^{dim+1} FMA + q-point op

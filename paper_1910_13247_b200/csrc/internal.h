@@ -60,6 +60,8 @@ enum Variant {
   kVariantGeneral = 1,  // 12-sweep collocation kernel, any dim/k/geometry
   kVariantCartTile = 2, // Cartesian constant-coefficient 3D tile kernel (slab form)
   kVariantCartPlane = 3, // Cartesian constant-coefficient 3D, 2D-first / z-last form
+  kVariantDG = 4,        // mf_create_dg (reported by mf_get_info)
+  kVariantHex = 5,       // mf_create_hex (reported by mf_get_info)
 };
 
 // Kernel launchers (return cudaError_t of the launch).
@@ -131,6 +133,31 @@ cudaError_t launch_cheb_init_f(const float *r, const float *dinv, float c0, floa
                                cudaStream_t s, int64_t *launches);
 cudaError_t launch_cheb_step_f(const float *r, const float *ax, const float *dinv, float c1, float c2, float *x,
                                float *d, int64_t n, cudaStream_t s, int64_t *launches);
+
+// unstructured hex operator (mf_create_hex; kernels_general.cu), device pointers
+constexpr int32_t kHexDirichlet = INT32_MIN;  // cell_dofs entry of a Dirichlet DoF
+struct HexDev {
+  int64_t ncells, ndofs, ndir;
+  const int32_t *cell_dofs;  // [ncells][(k+1)^3]: >= 0 DoF, kHexDirichlet, else -1 - line
+  const int32_t *line_ptr, *line_dof;  // constraint lines (Dirichlet entries removed)
+  const double *line_w;
+  const uint8_t *cell_lines;  // 1 if the cell has a constraint-line entry
+  const double *metric;       // [6][ncells][(k+1)^3]
+  const int32_t *dir;         // Dirichlet DoFs
+};
+cudaError_t launch_hex_metric(int k, const Tables &t, const double *V, const int32_t *CV, int64_t ncells,
+                              int coeff_kind, double coeff, double *metric, int *bad, cudaStream_t s,
+                              int64_t *launches);
+// dst must be zero; adds the cell contributions and writes the identity rows
+cudaError_t launch_apply_hex(int k, const Tables &t, const HexDev &h, const double *src, double *dst,
+                             cudaStream_t s, int64_t *launches);
+// diag must be zero
+cudaError_t launch_diagonal_hex(int k, const Tables &t, const HexDev &h, double *diag, cudaStream_t s,
+                                int64_t *launches);
+cudaError_t launch_hex_set(const HexDev &h, double *x, double value, cudaStream_t s, int64_t *launches);
+// DoF numbering of a conforming hex mesh (hex_dofs.cpp)
+mf_status hex_number_dofs(int k, int64_t n_cells, const int32_t *cell_vertices, int32_t *cell_dofs,
+                          int64_t *n_dofs, uint8_t *is_boundary, int64_t capacity, std::string *err);
 
 constexpr int kDotBlocks = 592;  // 4 x 148 SMs
 

@@ -1212,3 +1212,363 @@ cudaError_t launch_set_constrained(const Geo &g, double *x, double value, cudaSt
 }
 
 }  // namespace mf
+
+// ---------------------------------------------------------------------------
+// General unstructured hexahedral meshes (§3.1,
+// P:776-781 §3.5; R21, R22).  Same a3-a7 arithmetic as the stored-metric
+// path of k_apply_general; the gather reads the cell's DoF indices from cell_dofs
+// (int32, cell-major, coalesced) instead of computing them from brick coordinates,
+// and resolves a constraint line -- a hanging node, u = sum_j w_j u[dof_j] -- in the
+// gather and its transpose in the scatter (the paper's "constraints applied inside
+// the matrix-free loop").  Dirichlet entries read zero and receive nothing; their
+// identity rows are one extra pass over the Dirichlet list.
+namespace mf {
+
+// metric of the trilinear map (R21): thread = (cell, Gauss point);
+// G = c(x_q) w_q det J J^-1 J^-T, J[a][e] = d x_a / d xi_e, SoA [comp][cell][q]
+template <int K>
+__global__ void k_hex_metric(const __grid_constant__ Tables t, const double *__restrict__ V,
+                             const int32_t *__restrict__ CV, int64_t ncells, int coeff_kind, double coeff,
+                             double *__restrict__ metric, int *bad) {
+  constexpr int N = K + 1, NQ = N * N * N;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= ncells * NQ) return;
+  const int64_t cell = idx / NQ;
+  const int q = (int)(idx - cell * NQ);
+  const double xi[3] = {t.xi[q % N], t.xi[(q / N) % N], t.xi[q / (N * N)]};
+  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, x[3] = {0, 0, 0};
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const int c[3] = {v & 1, (v >> 1) & 1, v >> 2};
+    double f[3], df[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      f[d] = c[d] ? xi[d] : 1.0 - xi[d];
+      df[d] = c[d] ? 1.0 : -1.0;
+    }
+    const double Nv = f[0] * f[1] * f[2];
+    const double dN[3] = {df[0] * f[1] * f[2], f[0] * df[1] * f[2], f[0] * f[1] * df[2]};
+    const int64_t vid = CV[cell * 8 + v];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double X = V[vid * 3 + a];
+      x[a] += X * Nv;
+#pragma unroll
+      for (int e = 0; e < 3; ++e) J[a][e] += X * dN[e];
+    }
+  }
+  const double C00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], C01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+               C02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  const double det = J[0][0] * C00 + J[0][1] * C01 + J[0][2] * C02;
+  if (!(det > 0.0)) atomicExch(bad, 1);
+  // J^-1 = adj(J) / det, adj(J)[e][a] = cofactor[a][e]
+  double Ji[3][3];
+  Ji[0][0] = C00 / det;
+  Ji[1][0] = C01 / det;
+  Ji[2][0] = C02 / det;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+  const double c = coeff_kind == MF_COEFF_VARIABLE ? coeff_var(x, 3) : coeff;
+  const double f = c * t.w[q % N] * t.w[(q / N) % N] * t.w[q / (N * N)] * det;
+  const int ab[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  const int64_t stride = ncells * NQ;
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    const int a = ab[m][0], b = ab[m][1];
+    metric[m * stride + idx] = f * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+  }
+}
+
+__device__ __forceinline__ double hex_gather(const HexDev &h, const double *__restrict__ src, int32_t d) {
+  if (d >= 0) return __ldg(src + d);
+  if (d == kHexDirichlet) return 0.0;
+  const int l = -1 - d;
+  double v = 0.0;
+  for (int j = __ldg(h.line_ptr + l), e = __ldg(h.line_ptr + l + 1); j < e; ++j)
+    v = fma(__ldg(h.line_w + j), __ldg(src + __ldg(h.line_dof + j)), v);
+  return v;
+}
+
+__device__ __forceinline__ void hex_scatter(const HexDev &h, double *dst, int32_t d, double v) {
+  if (d >= 0) {
+    atomicAdd(dst + d, v);
+  } else if (d != kHexDirichlet) {
+    const int l = -1 - d;
+    for (int j = __ldg(h.line_ptr + l), e = __ldg(h.line_ptr + l + 1); j < e; ++j)
+      atomicAdd(dst + __ldg(h.line_dof + j), __ldg(h.line_w + j) * v);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_apply_hex(const __grid_constant__ Tables t, const __grid_constant__ HexDev h,
+                                                   const double *__restrict__ src, double *__restrict__ dst,
+                                                   int cpb) {
+  constexpr int DIM = 3, N = K + 1, NP = N * N, NV = NP * N;
+  constexpr int CS = 4 * NV;
+  extern __shared__ double sm[];
+  const int64_t ncells = h.ncells;
+  const int64_t cell0 = (int64_t)blockIdx.x * cpb;
+  // a3: gather through cell_dofs (constraint lines resolved here)
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int cl = idx / NV, i = idx - cl * NV;
+    const int64_t cell = cell0 + cl;
+    double v = 0.0;
+    if (cell < ncells) v = hex_gather(h, src, __ldg(h.cell_dofs + cell * NV + i));
+    sm[cl * CS + nidx<DIM, N>(i)] = v;
+  }
+  __syncthreads();
+  const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
+  const bool active = cl < cpb;
+  double *U = sm + cl * CS;
+  // a4: values at the Gauss points, then the reference gradient
+#pragma unroll
+  for (int e = 0; e < DIM; ++e) {
+    if (active) sweep_inplace<DIM, N, false>(t.S, U, e, p);
+    __syncthreads();
+  }
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) {
+      double a[N], b[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) a[i] = U[pen_off<DIM, N>(e, p, i)];
+      mat1d<N, false>(t.Co, a, b);
+      double *G = U + (e + 1) * NV;
+#pragma unroll
+      for (int i = 0; i < N; ++i) G[pen_off<DIM, N>(e, p, i)] = b[i];
+    }
+  }
+  __syncthreads();
+  // a5: the stored metric of the trilinear map
+  const int64_t stride = ncells * NV;
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int c2 = idx / NV, q = idx - c2 * NV;
+    const int64_t cell = cell0 + c2;
+    const bool ok = cell < ncells;
+    const double *Gm = h.metric + (ok ? cell * NV + q : 0);
+    double G[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) G[c] = ok ? __ldg(Gm + c * stride) : 0.0;
+    double *Uc = sm + c2 * CS;
+    const int qs = nidx<DIM, N>(q);
+    const double g0 = Uc[NV + qs], g1 = Uc[2 * NV + qs], g2 = Uc[3 * NV + qs];
+    Uc[NV + qs] = G[0] * g0 + G[1] * g1 + G[2] * g2;
+    Uc[2 * NV + qs] = G[1] * g0 + G[3] * g1 + G[4] * g2;
+    Uc[3 * NV + qs] = G[2] * g0 + G[4] * g1 + G[5] * g2;
+  }
+  __syncthreads();
+  // a6: transposed derivative and interpolation
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) sweep_inplace<DIM, N, true>(t.Co, U + (e + 1) * NV, e, p);
+  }
+  __syncthreads();
+  if (active) {
+    double a[N], b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int o = pen_off<DIM, N>(0, p, i);
+      a[i] = U[NV + o] + U[2 * NV + o] + U[3 * NV + o];
+    }
+    mat1d<N, true>(t.S, a, b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) U[pen_off<DIM, N>(0, p, i)] = b[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 1; e < DIM; ++e) {
+    if (active) sweep_inplace<DIM, N, true>(t.S, U, e, p);
+    __syncthreads();
+  }
+  // a7: scatter-add through cell_dofs (transpose of the constraint lines)
+  for (int idx = threadIdx.x; idx < cpb * NV; idx += blockDim.x) {
+    const int c2 = idx / NV, i = idx - c2 * NV;
+    const int64_t cell = cell0 + c2;
+    if (cell < ncells) hex_scatter(h, dst, __ldg(h.cell_dofs + cell * NV + i), sm[c2 * CS + nidx<DIM, N>(i)]);
+  }
+}
+
+// dst[dir] = src[dir] (identity rows), or = value when src is null
+__global__ void k_hex_identity(const int32_t *__restrict__ dir, int64_t n, const double *__restrict__ src,
+                               double *__restrict__ dst, double value) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = dir[i];
+    dst[d] = src ? src[d] : value;
+  }
+}
+
+// A_c[i][j] = sum_q grad_xi phi_i(q)^T G(q) grad_xi phi_j(q), brute force over q
+template <int K>
+__device__ double hex_entry(const Tables &t, const HexDev &h, int64_t cell, int i, int j) {
+  constexpr int N = K + 1, NV = N * N * N;
+  const int i0 = i % N, i1 = (i / N) % N, i2 = i / (N * N);
+  const int j0 = j % N, j1 = (j / N) % N, j2 = j / (N * N);
+  const int64_t stride = h.ncells * NV;
+  double s = 0.0;
+  for (int q = 0; q < NV; ++q) {
+    const int q0 = q % N, q1 = (q / N) % N, q2 = q / (N * N);
+    const double a[3] = {t.D[q0][i0] * t.S[q1][i1] * t.S[q2][i2], t.S[q0][i0] * t.D[q1][i1] * t.S[q2][i2],
+                         t.S[q0][i0] * t.S[q1][i1] * t.D[q2][i2]};
+    const double b[3] = {t.D[q0][j0] * t.S[q1][j1] * t.S[q2][j2], t.S[q0][j0] * t.D[q1][j1] * t.S[q2][j2],
+                         t.S[q0][j0] * t.S[q1][j1] * t.D[q2][j2]};
+    const double *Gm = h.metric + cell * NV + q;
+    const double G[6] = {__ldg(Gm), __ldg(Gm + stride), __ldg(Gm + 2 * stride), __ldg(Gm + 3 * stride),
+                         __ldg(Gm + 4 * stride), __ldg(Gm + 5 * stride)};
+    s += a[0] * (G[0] * b[0] + G[1] * b[1] + G[2] * b[2]) + a[1] * (G[1] * b[0] + G[3] * b[1] + G[4] * b[2]) +
+         a[2] * (G[2] * b[0] + G[4] * b[1] + G[5] * b[2]);
+  }
+  return s;
+}
+
+// diagonal of sum_c P_c^T A_c P_c: thread = (cell, local node i); on cells without
+// constraint lines only A_c[i][i]; on the others every pair (i, j) whose expansions
+// share a DoF m adds w_im w_jm A_c[i][j] to diag[m] (setup only)
+template <int K>
+__global__ void k_diag_hex(const __grid_constant__ Tables t, const __grid_constant__ HexDev h, double *diag) {
+  constexpr int N = K + 1, NV = N * N * N;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= h.ncells * NV) return;
+  const int64_t cell = idx / NV;
+  const int i = (int)(idx - cell * NV);
+  const int32_t di = h.cell_dofs[cell * NV + i];
+  if (di == kHexDirichlet) return;
+  if (!h.cell_lines[cell]) {
+    if (di >= 0) atomicAdd(diag + di, hex_entry<K>(t, h, cell, i, i));
+    return;
+  }
+  auto span = [&](int32_t d, int &b, int &e) {
+    if (d >= 0) {
+      b = 0;
+      e = 1;
+    } else {
+      b = h.line_ptr[-1 - d];
+      e = h.line_ptr[-d];
+    }
+  };
+  int bi, ei;
+  span(di, bi, ei);
+  for (int j = 0; j < NV; ++j) {
+    const int32_t dj = h.cell_dofs[cell * NV + j];
+    if (dj == kHexDirichlet) continue;
+    int bj, ej;
+    span(dj, bj, ej);
+    double Aij = 0.0;
+    bool have = false;
+    for (int a = bi; a < ei; ++a) {
+      const int32_t m = di >= 0 ? di : h.line_dof[a];
+      const double wm = di >= 0 ? 1.0 : h.line_w[a];
+      double s = 0.0;
+      bool hit = false;
+      for (int b = bj; b < ej; ++b) {
+        if ((dj >= 0 ? dj : h.line_dof[b]) == m) {
+          s += dj >= 0 ? 1.0 : h.line_w[b];
+          hit = true;
+        }
+      }
+      if (!hit) continue;
+      if (!have) {
+        Aij = hex_entry<K>(t, h, cell, i, j);
+        have = true;
+      }
+      atomicAdd(diag + m, wm * s * Aij);
+    }
+  }
+}
+
+template <int K>
+static cudaError_t hex_metric_k(const Tables &t, const double *V, const int32_t *CV, int64_t ncells, int ck,
+                                double cv, double *metric, int *bad, cudaStream_t s) {
+  constexpr int NQ = (K + 1) * (K + 1) * (K + 1);
+  const int64_t n = ncells * NQ;
+  if (n == 0) return cudaSuccess;
+  k_hex_metric<K><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(t, V, CV, ncells, ck, cv, metric, bad);
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t hex_apply_k(const Tables &t, const HexDev &h, const double *src, double *dst, cudaStream_t s) {
+  constexpr int N = K + 1, NP = N * N, NV = NP * N;
+  int cpb = 256 / NP;
+  while (cpb > 1 && cpb * 4 * NV * 8 > 48 * 1024) --cpb;
+  if (cpb < 1) cpb = 1;
+  const int threads = ((cpb * NP + 31) / 32) * 32;
+  const int64_t blocks = (h.ncells + cpb - 1) / cpb;
+  if (blocks == 0) return cudaSuccess;
+  k_apply_hex<K><<<(unsigned)blocks, threads, (size_t)cpb * 4 * NV * sizeof(double), s>>>(t, h, src, dst, cpb);
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t hex_diag_k(const Tables &t, const HexDev &h, double *diag, cudaStream_t s) {
+  constexpr int NV = (K + 1) * (K + 1) * (K + 1);
+  const int64_t n = h.ncells * NV;
+  if (n == 0) return cudaSuccess;
+  k_diag_hex<K><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(t, h, diag);
+  return cudaGetLastError();
+}
+
+#define MF_HEX_DISPATCH(CALL)      \
+  switch (k) {                     \
+    case 1: return CALL(1);        \
+    case 2: return CALL(2);        \
+    case 3: return CALL(3);        \
+    case 4: return CALL(4);        \
+    case 5: return CALL(5);        \
+    case 6: return CALL(6);        \
+    case 7: return CALL(7);        \
+    case 8: return CALL(8);        \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_hex_metric(int k, const Tables &t, const double *V, const int32_t *CV, int64_t ncells,
+                              int coeff_kind, double coeff, double *metric, int *bad, cudaStream_t s,
+                              int64_t *launches) {
+  ++*launches;
+#define MF_C(KK) hex_metric_k<KK>(t, V, CV, ncells, coeff_kind, coeff, metric, bad, s)
+  MF_HEX_DISPATCH(MF_C)
+#undef MF_C
+}
+
+static cudaError_t hex_identity(const HexDev &h, const double *src, double *dst, double value, cudaStream_t s,
+                                int64_t *launches) {
+  if (h.ndir == 0) return cudaSuccess;
+  ++*launches;
+  int64_t b = (h.ndir + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  k_hex_identity<<<(unsigned)b, 256, 0, s>>>(h.dir, h.ndir, src, dst, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_hex(int k, const Tables &t, const HexDev &h, const double *src, double *dst,
+                             cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  cudaError_t e = [&]() -> cudaError_t {
+#define MF_C(KK) hex_apply_k<KK>(t, h, src, dst, s)
+    MF_HEX_DISPATCH(MF_C)
+#undef MF_C
+  }();
+  if (e != cudaSuccess) return e;
+  return hex_identity(h, src, dst, 0.0, s, launches);
+}
+
+cudaError_t launch_diagonal_hex(int k, const Tables &t, const HexDev &h, double *diag, cudaStream_t s,
+                                int64_t *launches) {
+  ++*launches;
+  cudaError_t e = [&]() -> cudaError_t {
+#define MF_C(KK) hex_diag_k<KK>(t, h, diag, s)
+    MF_HEX_DISPATCH(MF_C)
+#undef MF_C
+  }();
+  if (e != cudaSuccess) return e;
+  return hex_identity(h, nullptr, diag, 1.0, s, launches);
+}
+
+cudaError_t launch_hex_set(const HexDev &h, double *x, double value, cudaStream_t s, int64_t *launches) {
+  return hex_identity(h, nullptr, x, value, s, launches);
+}
+
+}  // namespace mf

@@ -67,13 +67,21 @@ class Info(ctypes.Structure):
                 ("bytes_algorithmic", ctypes.c_int64), ("flops_algorithmic", ctypes.c_double)]
 
 
+class HexMeshC(ctypes.Structure):
+    _fields_ = [("n_vertices", ctypes.c_int64), ("n_cells", ctypes.c_int64), ("n_dofs", ctypes.c_int64),
+                ("n_lines", ctypes.c_int64), ("n_dirichlet", ctypes.c_int64),
+                ("vertices", ctypes.c_void_p), ("cell_vertices", ctypes.c_void_p), ("cell_dofs", ctypes.c_void_p),
+                ("line_ptr", ctypes.c_void_p), ("line_dof", ctypes.c_void_p), ("line_w", ctypes.c_void_p),
+                ("dirichlet_dofs", ctypes.c_void_p)]
+
+
 EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_sizes", "mf_set_stream",
            "mf_apply", "mf_apply_host", "mf_diagonal", "mf_estimate_lambda_max", "mf_chebyshev",
            "mf_cg_solve", "mf_get_info", "mf_set_apply_variant", "mf_set_kernel_timing", "mf_kernel_timing",
            "mf_partition", "mf_mg_create", "mf_mg_destroy", "mf_mg_levels", "mf_mg_level_size", "mf_mg_level_op",
            "mf_mg_level_lambda", "mf_mg_prolongate", "mf_mg_restrict", "mf_mg_vcycle", "mf_mg_cg_solve",
            "mf_mg_set_stream", "mf_apply_f32", "mf_create_dg", "mf_hng_create", "mf_hng_destroy", "mf_hng_sizes",
-           "mf_hng_apply", "mf_hng_set_stream"]
+           "mf_hng_apply", "mf_hng_set_stream", "mf_create_hex", "mf_hex_number_dofs"]
 
 _lib = None
 
@@ -128,6 +136,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "mf_hng_sizes": [vp, i64p, i64p],
         "mf_hng_apply": [vp, vp, i64, vp, i64],
         "mf_hng_set_stream": [vp, vp],
+        "mf_create_hex": [ctypes.POINTER(HexMeshC), ctypes.c_int32, ctypes.POINTER(Coeff), ctypes.POINTER(vp)],
+        "mf_hex_number_dofs": [ctypes.c_int32, i64, vp, vp, i64p, vp, i64],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -346,6 +356,68 @@ class Operator:
         ms, n = ctypes.c_double(), ctypes.c_int64()
         _check(load().mf_kernel_timing(self._h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+
+def hex_number_dofs(cell_vertices: np.ndarray, degree: int):
+    """mf_hex_number_dofs (host only): DoF numbering of a conforming hex mesh.
+    Returns (cell_dofs [n_cells][(k+1)^3] int32, n_dofs, is_boundary [n_dofs] bool)."""
+    cv = np.ascontiguousarray(cell_vertices, dtype=np.int32)
+    nc = cv.shape[0]
+    cd = np.empty((nc, (degree + 1) ** 3), dtype=np.int32)
+    cap = cd.size + 1
+    bnd = np.empty(cap, dtype=np.uint8)
+    n = ctypes.c_int64()
+    _check(load().mf_hex_number_dofs(degree, nc, cv.ctypes.data, cd.ctypes.data, ctypes.byref(n),
+                                     bnd.ctypes.data, cap))
+    return cd, n.value, bnd[:n.value].astype(bool)
+
+
+class HexOperator(Operator):
+    """v = A u for continuous Q_k on a general unstructured hex mesh (mf_create_hex;
+    include/mf.h): trilinear cells, cell_dofs (>= 0 DoF, < 0 constraint line -1 - v),
+    constraint lines as (dof, weight) lists, Dirichlet DoFs with identity rows.  All
+    Operator methods except the brick-only ones (apply_f32, set_variant) apply."""
+
+    def __init__(self, vertices, cell_vertices, degree, cell_dofs, n_dofs, lines=(), dirichlet=(), coeff=1.0,
+                 device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1910_13247_b200 needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        L = load()
+        V = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+        CV = np.ascontiguousarray(cell_vertices, dtype=np.int32).reshape(-1, 8)
+        CD = np.ascontiguousarray(cell_dofs, dtype=np.int32).reshape(CV.shape[0], -1)
+        lp = np.zeros(len(lines) + 1, dtype=np.int32)
+        for i, line in enumerate(lines):
+            lp[i + 1] = lp[i] + len(line)
+        ld = np.array([d for line in lines for d, _ in line] or [0], dtype=np.int32)
+        lw = np.array([w for line in lines for _, w in line] or [0.0], dtype=np.float64)
+        D = np.ascontiguousarray(np.asarray(dirichlet, dtype=np.int64).reshape(-1), dtype=np.int32)
+        D = D if D.size else np.zeros(1, dtype=np.int32)
+        m = HexMeshC()
+        m.n_vertices, m.n_cells, m.n_dofs = V.shape[0], CV.shape[0], int(n_dofs)
+        m.n_lines, m.n_dirichlet = len(lines), len(np.asarray(dirichlet).reshape(-1))
+        m.vertices, m.cell_vertices, m.cell_dofs = V.ctypes.data, CV.ctypes.data, CD.ctypes.data
+        m.line_ptr, m.line_dof, m.line_w, m.dirichlet_dofs = lp.ctypes.data, ld.ctypes.data, lw.ctypes.data, D.ctypes.data
+        c = Coeff()
+        if isinstance(coeff, str):
+            assert coeff == "variable"
+            c.kind, c.value = 1, 0.0
+        else:
+            c.kind, c.value = 0, float(coeff)
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        self._uid = None
+        with torch.cuda.device(device):
+            h = ctypes.c_void_p()
+            _check(L.mf_create_hex(ctypes.byref(m), degree, ctypes.byref(c), ctypes.byref(h)))
+        self._h = h
+        self.dim, self.degree, self.mesh = 3, degree, None
+        self.n_local = self.n_global = self.n_owned = int(n_dofs)
+        self.first_global = 0
 
 
 class Multigrid:
