@@ -448,6 +448,28 @@ __host__ __device__ constexpr int cell3_chunk();
 template <int K, int GEOM, class T>
 __host__ __device__ constexpr size_t cell3_smem_bytes();
 
+// unstructured hex meshes (GEOM 3): gather through cell_dofs, resolving a constraint
+// line (hanging node) u = sum_j w_j u[dof_j]; the scatter adds the transpose
+__device__ __forceinline__ double hex_gather(const HexDev &h, const double *__restrict__ src, int32_t d) {
+  if (d >= 0) return __ldg(src + d);
+  if (d == kHexDirichlet) return 0.0;
+  const int l = -1 - d;
+  double v = 0.0;
+  for (int j = __ldg(h.line_ptr + l), e = __ldg(h.line_ptr + l + 1); j < e; ++j)
+    v = fma(__ldg(h.line_w + j), __ldg(src + __ldg(h.line_dof + j)), v);
+  return v;
+}
+
+__device__ __forceinline__ void hex_scatter(const HexDev &h, double *dst, int32_t d, double v) {
+  if (d >= 0) {
+    atomicAdd(dst + d, v);
+  } else if (d != kHexDirichlet) {
+    const int l = -1 - d;
+    for (int j = __ldg(h.line_ptr + l), e = __ldg(h.line_ptr + l + 1); j < e; ++j)
+      atomicAdd(dst + __ldg(h.line_dof + j), __ldg(h.line_w + j) * v);
+  }
+}
+
 // sizeof(T)-byte cp.async (zero-fill when !ok)
 template <class T>
 __device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
@@ -463,8 +485,8 @@ __device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
 template <int K, int GEOM, class T = double>
 __host__ __device__ constexpr int cell3_cpb() {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
-  constexpr int per_cell = (int)sizeof(T) * (3 + (GEOM == 2 ? 6 : 0)) * NV;
-  int c = (GEOM == 2 ? 128 : 256) / NP;
+  constexpr int per_cell = (int)sizeof(T) * (3 + (GEOM >= 2 ? 6 : 0)) * NV;
+  int c = (GEOM >= 2 ? 128 : 256) / NP;
   while (c > 1 && c * per_cell > 48 * 1024) --c;
   return c < 1 ? 1 : c;
 }
@@ -481,20 +503,20 @@ __host__ __device__ constexpr int cell3_chunk() {
 }
 template <int K, int GEOM, class T>
 __host__ __device__ constexpr size_t cell3_smem_bytes() {
-  return sizeof(T) * (size_t)(cell3_ms_off<K, GEOM, T>() + (GEOM == 2 ? 6 * cell3_chunk<K, GEOM, T>() : 0));
+  return sizeof(T) * (size_t)(cell3_ms_off<K, GEOM, T>() + (GEOM >= 2 ? 6 * cell3_chunk<K, GEOM, T>() : 0));
 }
 
 template <int K, int GEOM, class T>
 __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typename TabOf<T>::type t,
                                                      const __grid_constant__ Geo g, const T *__restrict__ src,
                                                      T *__restrict__ dst, const T *__restrict__ metric,
-                                                     int64_t cbeg, int64_t cend) {
+                                                     int64_t cbeg, int64_t cend, const __grid_constant__ HexDev hx) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   constexpr int CS = 3 * NV;  // U, G0, G1 per cell (the z-gradient lives in registers)
   constexpr int cpb = cell3_cpb<K, GEOM, T>();
   extern __shared__ __align__(16) unsigned char smraw[];
   T *const sm = reinterpret_cast<T *>(smraw);
-  const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
+  const int64_t ncells = GEOM == 3 ? hx.ncells : g.nc[0] * g.nc[1] * g.nc[2];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
   const bool active = cl < cpb;
   const int64_t cell0 = cbeg + (int64_t)blockIdx.x * cpb, cell = cell0 + cl;  // cells [cbeg, cend)
@@ -506,7 +528,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
   T *Ms = sm + cell3_ms_off<K, GEOM, T>();  // 16-byte aligned (bulk-copy destination)
   __shared__ alignas(8) unsigned long long mbar;
   bool bulk = false;
-  if (GEOM == 2) {
+  if (GEOM >= 2) {
     constexpr int CH = cell3_chunk<K, GEOM, T>();  // padded component chunk (16-byte multiple)
     const int64_t cstride = ncells * NV;
     const int64_t rem = cend - cell0;
@@ -554,8 +576,15 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
     o2[i] = pen_off<3, N>(2, p, i);
   }
   const int64_t Nx = g.N[0], plane = g.N[0] * g.N[1];
-  const CellInfo ci = cell_info<3, K>(g, valid ? cell : ncells, ncells);
+  const CellInfo ci = GEOM == 3 ? CellInfo{} : cell_info<3, K>(g, valid ? cell : ncells, ncells);
   T a[N], b[N];
+  int32_t hd[GEOM == 3 ? N : 1];  // hex: the DoF entries of this thread's x-pencil
+  if constexpr (GEOM == 3) {
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) hd[i] = __ldg(hx.cell_dofs + cell * NV + N * p + i);
+    }
+  }
 
   if constexpr (GEOM == 0) {
     // Cartesian box, constant coefficient: the Gauss(k+1)-exact Kronecker form of the
@@ -640,10 +669,14 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
   if (active) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      int64_t gi;
-      bool cons, owner;
-      node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
-      a[i] = (valid && !cons) ? __ldg(src + gi) : 0.0;
+      if constexpr (GEOM == 3) {
+        a[i] = valid ? (T)hex_gather(hx, reinterpret_cast<const double *>(src), hd[i]) : T(0);
+      } else {
+        int64_t gi;
+        bool cons, owner;
+        node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
+        a[i] = (valid && !cons) ? __ldg(src + gi) : 0.0;
+      }
     }
     mat1d<N, false>(t.S, a, b);
 #pragma unroll
@@ -676,7 +709,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
 #pragma unroll
     for (int i = 0; i < N; ++i) G1[o1[i]] = b[i];
   }
-  if (GEOM == 2) {
+  if (GEOM >= 2) {
     if (bulk) {
       const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
       asm volatile(
@@ -698,7 +731,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
     for (int i = 0; i < N; ++i) {
       const T gr0 = G0[o2[i]], gr1 = G1[o2[i]], gr2 = gz[i];
       T tt0, tt1, tt2;
-      if (GEOM == 2) {
+      if (GEOM >= 2) {
         T G[NGC];
 #pragma unroll
         for (int c = 0; c < NGC; ++c) G[c] = Gm[c * cell3_chunk<K, GEOM, T>() + NP * i];
@@ -754,13 +787,17 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
     mat1d<N, true>(t.S, a, b);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      int64_t gi;
-      bool cons, owner;
-      node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
-      if (cons) {
-        if (owner) dst[gi] = __ldg(src + gi);
+      if constexpr (GEOM == 3) {
+        hex_scatter(hx, reinterpret_cast<double *>(dst), hd[i], (double)b[i]);
       } else {
-        atomicAdd(dst + gi, b[i]);
+        int64_t gi;
+        bool cons, owner;
+        node_of<3, N>(ci, i + N * p, Nx, plane, gi, cons, owner);
+        if (cons) {
+          if (owner) dst[gi] = __ldg(src + gi);
+        } else {
+          atomicAdd(dst + gi, b[i]);
+        }
       }
     }
   }
@@ -797,7 +834,7 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
                           true);
       (void)attr;
       k_apply_cell3<K, GEOM, double><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric,
-                                                                                            cbeg, cend);
+                                                                                            cbeg, cend, HexDev{});
       return cudaGetLastError();
     }
   }
@@ -842,7 +879,7 @@ static cudaError_t launch_cell3_f32(const Geo &g, const TablesF &tf, const float
   (void)attr;
   if (b3 == 0) return cudaSuccess;
   k_apply_cell3<K, GEOM, float><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(tf, g, src, dst, metric, 0,
-                                                                                      ncells);
+                                                                                      ncells, HexDev{});
   return cudaGetLastError();
 }
 
@@ -1283,26 +1320,6 @@ __global__ void k_hex_metric(const __grid_constant__ Tables t, const double *__r
   }
 }
 
-__device__ __forceinline__ double hex_gather(const HexDev &h, const double *__restrict__ src, int32_t d) {
-  if (d >= 0) return __ldg(src + d);
-  if (d == kHexDirichlet) return 0.0;
-  const int l = -1 - d;
-  double v = 0.0;
-  for (int j = __ldg(h.line_ptr + l), e = __ldg(h.line_ptr + l + 1); j < e; ++j)
-    v = fma(__ldg(h.line_w + j), __ldg(src + __ldg(h.line_dof + j)), v);
-  return v;
-}
-
-__device__ __forceinline__ void hex_scatter(const HexDev &h, double *dst, int32_t d, double v) {
-  if (d >= 0) {
-    atomicAdd(dst + d, v);
-  } else if (d != kHexDirichlet) {
-    const int l = -1 - d;
-    for (int j = __ldg(h.line_ptr + l), e = __ldg(h.line_ptr + l + 1); j < e; ++j)
-      atomicAdd(dst + __ldg(h.line_dof + j), __ldg(h.line_w + j) * v);
-  }
-}
-
 template <int K>
 __global__ void __launch_bounds__(256) k_apply_hex(const __grid_constant__ Tables t, const __grid_constant__ HexDev h,
                                                    const double *__restrict__ src, double *__restrict__ dst,
@@ -1492,6 +1509,21 @@ static cudaError_t hex_metric_k(const Tables &t, const double *V, const int32_t 
 template <int K>
 static cudaError_t hex_apply_k(const Tables &t, const HexDev &h, const double *src, double *dst, cudaStream_t s) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
+  static const bool v1 = std::getenv("MF_HEX_V1") != nullptr;  // the shared-memory pencil kernel (comparisons)
+  if (!v1) {  // k_apply_cell3 with the cell_dofs gather / scatter and the TMA-staged metric
+    constexpr int c3 = cell3_cpb<K, 3>();
+    const int64_t b3 = (h.ncells + c3 - 1) / c3;
+    const size_t sm3 = cell3_smem_bytes<K, 3, double>();
+    static bool attr = (cudaFuncSetAttribute(k_apply_cell3<K, 3, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm3),
+                        true);
+    (void)attr;
+    if (b3 == 0) return cudaSuccess;
+    Geo g{};
+    k_apply_cell3<K, 3, double><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, h.metric, 0,
+                                                                                      h.ncells, h);
+    return cudaGetLastError();
+  }
   int cpb = 256 / NP;
   while (cpb > 1 && cpb * 4 * NV * 8 > 48 * 1024) --cpb;
   if (cpb < 1) cpb = 1;
