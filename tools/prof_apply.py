@@ -18,8 +18,15 @@ ap.add_argument("--variant", default="auto")
 ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
 nc, k, geom, coeff, _ = CONFIGS[a.config]
-op = Operator(nc, k, geometry=geom, coeff=coeff)
-op.set_variant(a.variant)
+if geom == "hex":
+    from bench import make_hex_operator
+
+    op, _ = make_hex_operator(nc, k, coeff, torch.cuda.current_device())
+elif geom == "dg":
+    op = Operator(nc, k, coeff=coeff, discretization="dg")
+else:
+    op = Operator(nc, k, geometry=geom, coeff=coeff)
+    op.set_variant(a.variant)
 x = torch.from_numpy(synth.vector(op.n_local, 0)).cuda()
 y = torch.empty_like(x)
 for _ in range(a.reps):
