@@ -14,7 +14,9 @@
 // read from global memory; DG DoFs are cell-major, so a neighbour's pencil is one
 // contiguous or strided run inside its cell block), then the two tangential masses,
 // and accumulates.  Every DoF belongs to one cell: plain stores, no atomics.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -29,6 +31,12 @@ namespace {
 struct DGParams {
   double B[3][6][kMaxN][kMaxN];
   double M[3][kMaxN][kMaxN];
+  // the face couplings have rank 2 on GLL nodes (the trace of a Lagrange basis is a unit
+  // vector): B[e][4] = e_0 a4^T + g4 e_k^T, B[e][5] = e_k a5^T + g5 e_0^T
+  double a4[3][kMaxN], g4[3][kMaxN], a5[3][kMaxN], g5[3][kMaxN];
+  // the boundary self blocks differ from the interior one by symmetric rank-2 terms:
+  // B[e][1] = B[e][0] + e_0 bl^T + bl e_0^T, B[e][2] = B[e][0] + e_k bh^T + bh e_k^T
+  double bl[3][kMaxN], bh[3][kMaxN];
   int64_t nc[3];
 };
 
@@ -146,6 +154,237 @@ __global__ void __launch_bounds__(256) k_apply_dg(const __grid_constant__ DGPara
   }
 }
 
+// the boundary corrections of a self block (warp-divergent only on boundary cells)
+template <int N>
+__device__ __forceinline__ void self_bnd(const double (&bl)[kMaxN], const double (&bh)[kMaxN], bool lo, bool hi,
+                                         const double *a, double *b) {
+  if (lo) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(bl[j], a[j], s);
+    b[0] += s;
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = fma(bl[i], a[0], b[i]);
+  }
+  if (hi) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(bh[j], a[j], s);
+    b[N - 1] += s;
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = fma(bh[i], a[N - 1], b[i]);
+  }
+}
+
+// Kronecker-sum form with rank-2 face couplings (the default; k_apply_dg above is kept as
+// MF_DG_V1).  With u_K the cell's values (x fastest) and, for direction e, the lower /
+// upper neighbour couplings B4 u_nb = e_0 (a4 . u_nb) + g4 u_nb[k] and
+// B5 u_nb = e_k (a5 . u_nb) + g5 u_nb[0] along e, the three terms share their masses:
+//   Z (thread = z-pencil):  W = M_z u,  Z = B_z u (+ z-neighbour couplings)
+//   Y (thread = y-pencil):  C = M_y W,  E = B_y W + M_y Z   (y-neighbours' traces
+//                           a.u_nb and u_nb[face] taken first, then M_z along z)
+//   X (thread = x-pencil):  v = B_x C + M_x E               (x-neighbours' traces
+//                           transformed by M_z, then M_y)
+// 7 one-dimensional products per cell instead of 9, rank-2 instead of dense neighbour
+// products, two barriers, and 2 (k+1)^3 + 12 (k+1)^2 doubles of shared memory per cell.
+template <int K>
+__global__ void __launch_bounds__(256) k_apply_dg2(const __grid_constant__ DGParams D, const double *__restrict__ src,
+                                                   double *__restrict__ dst, int cpb) {
+  constexpr int N = K + 1, NP = N * N, NV = NP * N, CS = 2 * NV + 12 * NP;
+  extern __shared__ double sm[];
+  const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
+  const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
+  const int64_t cell = (int64_t)blockIdx.x * cpb + cl;
+  const bool valid = cl < cpb && cell < ncells;
+  // the y / z masses, read by thread-dependent rows in the trace transforms: shared
+  // memory (a per-thread row of the parameter bank would serialise on the constant cache)
+  double *My = sm + cpb * CS, *Mz = My + NP;
+  for (int i = threadIdx.x; i < 2 * NP; i += blockDim.x) My[i] = D.M[1 + i / NP][(i % NP) / N][i % N];
+  double *WC = sm + (valid ? cl : 0) * CS, *ZE = WC + NV;
+  // neighbour traces as (a . u_nb, u_nb[face]) pairs: TR[face][NP], face = y-lo, y-hi, x-lo,
+  // x-hi; T1[2][NP] the x-face pairs after M_z
+  double2 *TR = reinterpret_cast<double2 *>(ZE + NV), *T1 = TR + 4 * NP;
+  int64_t c[3] = {0, 0, 0};
+  if (valid) {
+    c[0] = cell % D.nc[0];
+    const int64_t r = cell / D.nc[0];
+    c[1] = r % D.nc[1];
+    c[2] = r / D.nc[1];
+  }
+  const int64_t sx = NV, sy = D.nc[0] * NV, sz = D.nc[0] * D.nc[1] * NV;
+  const double *uK = src + cell * NV;
+  const int pa = p % N, pb = p / N;
+  double a[N], w[N], b[N];
+  // ---- Z: thread (x, y) = (pa, pb) on its z-pencil; traces of the x / y neighbours
+  if (valid) {
+#pragma unroll
+    for (int z = 0; z < N; ++z) a[z] = __ldg(uK + p + NP * z);
+    mv<N>(D.M[2], a, w);
+    const bool lo = c[2] == 0, hi = c[2] == D.nc[2] - 1;
+    mv<N>(D.B[2][0], a, b);
+    self_bnd<N>(D.bl[2], D.bh[2], lo, hi, a, b);
+    if (!lo) {
+      const double *un = uK - sz + p;
+      double s = 0.0;
+#pragma unroll
+      for (int z = 0; z < N; ++z) s = fma(D.a4[2][z], __ldg(un + NP * z), s);
+      const double f = __ldg(un + NP * K);
+      b[0] += s;
+#pragma unroll
+      for (int z = 0; z < N; ++z) b[z] = fma(D.g4[2][z], f, b[z]);
+    }
+    if (!hi) {
+      const double *un = uK + sz + p;
+      double s = 0.0;
+#pragma unroll
+      for (int z = 0; z < N; ++z) s = fma(D.a5[2][z], __ldg(un + NP * z), s);
+      const double f = __ldg(un);
+      b[K] += s;
+#pragma unroll
+      for (int z = 0; z < N; ++z) b[z] = fma(D.g5[2][z], f, b[z]);
+    }
+#pragma unroll
+    for (int z = 0; z < N; ++z) {
+      WC[p + NP * z] = w[z];
+      ZE[p + NP * z] = b[z];
+    }
+    // y-face traces at (x, z) = (pa, pb): a.u_nb along y and the face value
+    if (c[1] > 0) {
+      const double *un = uK - sy + pa + NP * pb;
+      double s = 0.0;
+#pragma unroll
+      for (int y = 0; y < N; ++y) s = fma(D.a4[1][y], __ldg(un + N * y), s);
+      TR[p] = make_double2(s, __ldg(un + N * K));
+    }
+    if (c[1] < D.nc[1] - 1) {
+      const double *un = uK + sy + pa + NP * pb;
+      double s = 0.0;
+#pragma unroll
+      for (int y = 0; y < N; ++y) s = fma(D.a5[1][y], __ldg(un + N * y), s);
+      TR[NP + p] = make_double2(s, __ldg(un));
+    }
+    // x-face traces at (y, z) = (pa, pb)
+    if (c[0] > 0) {
+      const double *un = uK - sx + N * pa + NP * pb;
+      double s = 0.0;
+#pragma unroll
+      for (int x = 0; x < N; ++x) s = fma(D.a4[0][x], __ldg(un + x), s);
+      TR[2 * NP + p] = make_double2(s, __ldg(un + K));
+    }
+    if (c[0] < D.nc[0] - 1) {
+      const double *un = uK + sx + N * pa + NP * pb;
+      double s = 0.0;
+#pragma unroll
+      for (int x = 0; x < N; ++x) s = fma(D.a5[0][x], __ldg(un + x), s);
+      TR[3 * NP + p] = make_double2(s, __ldg(un));
+    }
+  }
+  __syncthreads();
+  // ---- Y: thread (x, z) = (pa, pb) on its y-pencil
+  if (valid) {
+    const int base = pa + NP * pb;
+#pragma unroll
+    for (int y = 0; y < N; ++y) a[y] = WC[base + N * y];
+    double cc[N], e[N];
+    mv<N>(D.M[1], a, cc);
+    const bool lo = c[1] == 0, hi = c[1] == D.nc[1] - 1;
+    mv<N>(D.B[1][0], a, e);
+    self_bnd<N>(D.bl[1], D.bh[1], lo, hi, a, e);
+#pragma unroll
+    for (int y = 0; y < N; ++y) a[y] = ZE[base + N * y];
+    mv_acc<N>(D.M[1], a, e);
+    // y-neighbours: traces along z through M_z (row pb of M_z in registers)
+    double mz[N];
+#pragma unroll
+    for (int z = 0; z < N; ++z) mz[z] = Mz[N * pb + z];
+    if (!lo) {
+      double s = 0.0, f = 0.0;
+#pragma unroll
+      for (int z = 0; z < N; ++z) {
+        const double2 t = TR[pa + N * z];
+        s = fma(mz[z], t.x, s);
+        f = fma(mz[z], t.y, f);
+      }
+      e[0] += s;
+#pragma unroll
+      for (int y = 0; y < N; ++y) e[y] = fma(D.g4[1][y], f, e[y]);
+    }
+    if (!hi) {
+      double s = 0.0, f = 0.0;
+#pragma unroll
+      for (int z = 0; z < N; ++z) {
+        const double2 t = TR[NP + pa + N * z];
+        s = fma(mz[z], t.x, s);
+        f = fma(mz[z], t.y, f);
+      }
+      e[K] += s;
+#pragma unroll
+      for (int y = 0; y < N; ++y) e[y] = fma(D.g5[1][y], f, e[y]);
+    }
+#pragma unroll
+    for (int y = 0; y < N; ++y) {
+      WC[base + N * y] = cc[y];
+      ZE[base + N * y] = e[y];
+    }
+    // x-face traces (y, z) = (pa, pb): M_z along z
+#pragma unroll
+    for (int f2 = 0; f2 < 2; ++f2) {
+      if (f2 == 0 ? c[0] > 0 : c[0] < D.nc[0] - 1) {
+        double s = 0.0, f = 0.0;
+#pragma unroll
+        for (int z = 0; z < N; ++z) {
+          const double2 t = TR[(2 + f2) * NP + pa + N * z];
+          s = fma(mz[z], t.x, s);
+          f = fma(mz[z], t.y, f);
+        }
+        T1[f2 * NP + p] = make_double2(s, f);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- X: thread (y, z) = (pa, pb) on its x-pencil
+  if (valid) {
+    const int base = N * pa + NP * pb;
+#pragma unroll
+    for (int x = 0; x < N; ++x) a[x] = WC[base + x];
+    const bool lo = c[0] == 0, hi = c[0] == D.nc[0] - 1;
+    mv<N>(D.B[0][0], a, b);
+    self_bnd<N>(D.bl[0], D.bh[0], lo, hi, a, b);
+#pragma unroll
+    for (int x = 0; x < N; ++x) a[x] = ZE[base + x];
+    mv_acc<N>(D.M[0], a, b);
+    double my[N];
+#pragma unroll
+    for (int y = 0; y < N; ++y) my[y] = My[N * pa + y];
+    if (!lo) {
+      double s = 0.0, f = 0.0;
+#pragma unroll
+      for (int y = 0; y < N; ++y) {
+        const double2 t = T1[y + N * pb];
+        s = fma(my[y], t.x, s);
+        f = fma(my[y], t.y, f);
+      }
+      b[0] += s;
+#pragma unroll
+      for (int x = 0; x < N; ++x) b[x] = fma(D.g4[0][x], f, b[x]);
+    }
+    if (!hi) {
+      double s = 0.0, f = 0.0;
+#pragma unroll
+      for (int y = 0; y < N; ++y) {
+        const double2 t = T1[NP + y + N * pb];
+        s = fma(my[y], t.x, s);
+        f = fma(my[y], t.y, f);
+      }
+      b[K] += s;
+#pragma unroll
+      for (int x = 0; x < N; ++x) b[x] = fma(D.g5[0][x], f, b[x]);
+    }
+#pragma unroll
+    for (int x = 0; x < N; ++x) dst[cell * NV + base + x] = b[x];
+  }
+}
+
 __global__ void k_diag_dg(const __grid_constant__ DGParams D, int N, double *__restrict__ diag) {
   const int64_t NV = (int64_t)N * N * N, ncells = D.nc[0] * D.nc[1] * D.nc[2];
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ncells * NV;
@@ -220,12 +459,55 @@ void build_dg(const Geo &g, const Tables &t, DGParams *D) {
         D->B[e][4][i][j] = c * (0.5 * v0[i] * d1[j] / h - 0.5 * d0[i] / h * v1[j] - sig * v0[i] * v1[j]);
         D->B[e][5][i][j] = c * (-v1[i] * 0.5 * d0[j] / h + 0.5 * d1[i] / h * v0[j] - sig * v1[i] * v0[j]);
       }
+    // rank-2 factors (v0 = e_0, v1 = e_k on the GLL nodes)
+    for (int j = 0; j < N; ++j) {
+      D->a4[e][j] = c * (0.5 * d1[j] / h - sig * v1[j]);
+      D->g4[e][j] = -0.5 * c * d0[j] / h;
+      D->a5[e][j] = c * (-0.5 * d0[j] / h - sig * v0[j]);
+      D->g5[e][j] = 0.5 * c * d1[j] / h;
+      D->bl[e][j] = 0.5 * c * d0[j] / h;
+      D->bh[e][j] = -0.5 * c * d1[j] / h;
+    }
   }
+}
+
+// max |B[e][4|5] - rank-2 form| relative to max |B|: the kernel's precondition
+double dg_rank2_defect(const DGParams &D, int N) {
+  double err = 0.0, big = 0.0;
+  for (int e = 0; e < 3; ++e)
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        const double r4 = (i == 0 ? D.a4[e][j] : 0.0) + (j == N - 1 ? D.g4[e][i] : 0.0);
+        const double r5 = (i == N - 1 ? D.a5[e][j] : 0.0) + (j == 0 ? D.g5[e][i] : 0.0);
+        err = std::max(err, std::max(std::fabs(D.B[e][4][i][j] - r4), std::fabs(D.B[e][5][i][j] - r5)));
+        big = std::max(big, std::max(std::fabs(D.B[e][4][i][j]), std::fabs(D.B[e][5][i][j])));
+        const double cl = (i == 0 ? D.bl[e][j] : 0.0) + (j == 0 ? D.bl[e][i] : 0.0);
+        const double ch = (i == N - 1 ? D.bh[e][j] : 0.0) + (j == N - 1 ? D.bh[e][i] : 0.0);
+        err = std::max(err, std::fabs(D.B[e][1][i][j] - D.B[e][0][i][j] - cl));
+        err = std::max(err, std::fabs(D.B[e][2][i][j] - D.B[e][0][i][j] - ch));
+        err = std::max(err, std::fabs(D.B[e][3][i][j] - D.B[e][0][i][j] - cl - ch));
+        big = std::max(big, std::fabs(D.B[e][0][i][j]));
+      }
+  return big > 0.0 ? err / big : err;
 }
 
 template <int K>
 cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaStream_t s) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
+  static const bool v1 = std::getenv("MF_DG_V1") != nullptr;
+  if (!v1 && dg_rank2_defect(D, N) <= 1e-14) {
+    constexpr int CS = 2 * NV + 12 * NP;
+    const int cpb = 256 / NP;
+    const size_t smem = (size_t)(cpb * CS + 2 * NP) * sizeof(double);
+    static bool attr2 = (cudaFuncSetAttribute(k_apply_dg2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                         true);
+    (void)attr2;
+    const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
+    const int64_t blocks = (ncells + cpb - 1) / cpb;
+    if (blocks == 0) return cudaSuccess;
+    k_apply_dg2<K><<<(unsigned)blocks, ((cpb * NP + 31) / 32) * 32, smem, s>>>(D, src, dst, cpb);
+    return cudaGetLastError();
+  }
   int cpb = 256 / NP;
   while (cpb > 1 && (3 * cpb + 2) * NV * 8 > 96 * 1024) --cpb;
   if (cpb < 1) cpb = 1;

@@ -26,6 +26,10 @@ CASES = [
     dict(n_cells=(2, 2, 1), k=4),
     dict(n_cells=(1, 1, 1), k=5),
     dict(n_cells=(2, 1, 2), k=6),
+    dict(n_cells=(2, 2, 1), k=7),
+    dict(n_cells=(1, 2, 1), k=8),
+    dict(n_cells=(5, 4, 3), k=2, upper=(2.0, 1.0, 0.5)),   # interior cells in every direction, ragged block
+    dict(n_cells=(4, 3, 5), k=4),
 ]
 
 
