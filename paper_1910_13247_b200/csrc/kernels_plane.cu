@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
   Item G = item_of(item);
   prefetch(G, G.cz_begin, 0);
   T pcar[K + 1], qcar[K + 1], vcar[K + 1];  // owned columns i = 0..K-1, [K] = edge column
+  bool dep_done = false;
 
   while (true) {
     const int cz_begin = G.cz_begin, cz_end = G.cz_end, chunk = G.chunk;
@@ -280,6 +281,10 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
       }
       __syncthreads();
       // ---- column phase: prefetch the next layer, then gather P, Q and sweep in z
+      if (!dep_done) {  // the init grid (zeroed shared planes, identity rows) is complete
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        dep_done = true;
+      }
       if (!last) {
         prefetch(G, cz + 1, 1);
       } else if (next < nitems) {
@@ -399,8 +404,22 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T
   if (items == 0) return cudaSuccess;
   ++*launches;
   const int blocks = std::min(items, slots);
-  k_apply_plane<K, TX, TY, ISO, T><<<blocks, S::NT, S::template smem<T>(), s>>>(P, src, dst);
-  return cudaGetLastError();
+  if (part == 2) {
+    k_apply_plane<K, TX, TY, ISO, T><<<blocks, S::NT, S::template smem<T>(), s>>>(P, src, dst);
+    return cudaGetLastError();
+  }
+  // programmatic dependent launch on the init kernel: the blocks start while it runs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(S::NT);
+  cfg.dynamicSmemBytes = S::template smem<T>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_apply_plane<K, TX, TY, ISO, T>, P, src, dst);
 }
 
 bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }

@@ -135,6 +135,9 @@ template <class T>
 static __global__ void __launch_bounds__(256) k_tile_init(const __grid_constant__ TileParams P,
                                                            const __grid_constant__ PlaneSet ps,
                                                            const T *__restrict__ src, T *__restrict__ dst) {
+  // the apply kernel that follows may start now (programmatic dependent launch): it reads
+  // src and builds its first faces, and waits for this grid before its first dst write
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // one warp per line of a plane (x-plane: line gz, nodes gy; y-plane: line gz,
   // nodes gx; z-plane: line gy, nodes gx), warps grid-stride over all lines
   const int Nx = (int)P.Nx, Ny = (int)P.Ny, Nz = (int)P.Nz;
