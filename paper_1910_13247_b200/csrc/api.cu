@@ -533,8 +533,8 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
 
 static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
   if (op->hex) {
-    CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
     STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
     CUDA_TRY(launch_apply_hex(op->g.k, op->t, op->hx, src, dst, op->stream, &op->launches));
     return timing_mark(op);
   }
@@ -554,8 +554,8 @@ static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
     CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches));
     STATUS_TRY(timing_mark(op));
   } else {
+    STATUS_TRY(timing_mark(op));  // (zeroing + kernel, as the plane path's init + kernel)
     CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
-    STATUS_TRY(timing_mark(op));
     CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches));
     STATUS_TRY(timing_mark(op));
   }

@@ -510,6 +510,31 @@ template <int K, int GEOM, class T>
 __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typename TabOf<T>::type t,
                                                      const __grid_constant__ Geo g, const T *__restrict__ src,
                                                      T *__restrict__ dst, const T *__restrict__ metric,
+                                                     int64_t cbeg, int64_t cend, const __grid_constant__ HexDev hx);
+
+// launch k_apply_cell3 as a programmatic dependent of the preceding (zeroing) kernel
+template <int K, int GEOM>
+static cudaError_t launch_cell3_pdl(unsigned blocks, unsigned threads, size_t smem, cudaStream_t s, const Tables &t,
+                                    const Geo &g, const double *src, double *dst, const double *metric, int64_t cbeg,
+                                    int64_t cend, const HexDev &hx) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool off = std::getenv("MF_NO_PDL") != nullptr;  // plain stream order (comparisons)
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, k_apply_cell3<K, GEOM, double>, t, g, src, dst, metric, cbeg, cend, hx);
+}
+
+template <int K, int GEOM, class T>
+__global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typename TabOf<T>::type t,
+                                                     const __grid_constant__ Geo g, const T *__restrict__ src,
+                                                     T *__restrict__ dst, const T *__restrict__ metric,
                                                      int64_t cbeg, int64_t cend, const __grid_constant__ HexDev hx) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   constexpr int CS = 3 * NV;  // U, G0, G1 per cell (the z-gradient lives in registers)
@@ -639,6 +664,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
       for (int i = 0; i < N; ++i) B1[o1[i]] = b[i];
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the zeroing grid is complete
     if (active && valid) {  // x, then scatter-add and identity rows
 #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -780,7 +806,9 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
   // 8: S^T along y
   if (active) sweep_inplace<3, N, true>(t.S, U, 1, p);
   __syncthreads();
-  // 9: S^T along x in registers; scatter-add, identity rows by their owner cell
+  // 9: S^T along x in registers; scatter-add, identity rows by their owner cell (after the
+  // zeroing grid this kernel may overlap under programmatic dependent launch)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (valid) {
 #pragma unroll
     for (int i = 0; i < N; ++i) a[i] = U[o0[i]];
@@ -833,9 +861,8 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3),
                           true);
       (void)attr;
-      k_apply_cell3<K, GEOM, double><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, metric,
-                                                                                            cbeg, cend, HexDev{});
-      return cudaGetLastError();
+      return launch_cell3_pdl<K, GEOM>((unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s, t, g, src, dst, metric, cbeg,
+                                       cend, HexDev{});
     }
   }
   if (cbeg != 0 || cend != ncells) return cudaErrorNotSupported;
@@ -1520,9 +1547,8 @@ static cudaError_t hex_apply_k(const Tables &t, const HexDev &h, const double *s
     (void)attr;
     if (b3 == 0) return cudaSuccess;
     Geo g{};
-    k_apply_cell3<K, 3, double><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(t, g, src, dst, h.metric, 0,
-                                                                                      h.ncells, h);
-    return cudaGetLastError();
+    return launch_cell3_pdl<K, 3>((unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s, t, g, src, dst, h.metric, 0,
+                                  h.ncells, h);
   }
   int cpb = 256 / NP;
   while (cpb > 1 && cpb * 4 * NV * 8 > 48 * 1024) --cpb;

@@ -26,6 +26,8 @@
 //                 (cp.async), z-sweep in even-odd form with the plane-0 values
 //                 carried from the previous layer, store the k finished planes.
 // Shared tile-edge / chunk-plane nodes: init kernel + FP64 atomics (tile_common.cuh).
+#include <cstdlib>
+
 #include "tile_common.cuh"
 
 namespace mf {
@@ -418,7 +420,8 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool off = std::getenv("MF_NO_PDL") != nullptr;  // plain stream order (comparisons)
+  cfg.numAttrs = off ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, k_apply_plane<K, TX, TY, ISO, T>, P, src, dst);
 }
 

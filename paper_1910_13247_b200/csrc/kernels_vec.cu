@@ -16,6 +16,8 @@ static unsigned grid_for(int64_t n, int threads = 256) {
 }
 
 __global__ void k_zero(double *x, int64_t n) {
+  // a dependent apply kernel may start its gather now (it waits for this grid before writing)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = 0.0;
 }
