@@ -132,3 +132,47 @@ def test_hex_errors(torch):
     with pytest.raises(MFError) as e:
         _op(dict(m, cell_dofs=cd))
     assert e.value.name == "MF_ERR_ARGUMENT"
+
+
+def _support_coords(V, C, cd, n, k):
+    """Physical coordinates of every DoF (trilinear map of the GLL nodes), test-side numpy."""
+    import oracle
+
+    nodes = oracle.gll(k)
+    N = k + 1
+    loc = np.array([[i % N, (i // N) % N, i // (N * N)] for i in range(N ** 3)])
+    xi = nodes[loc]  # [nv][3]
+    corners = np.array([[v & 1, (v >> 1) & 1, v >> 2] for v in range(8)], dtype=np.float64)
+    Nv = np.prod(np.where(corners[None, :, :] == 1, xi[:, None, :], 1.0 - xi[:, None, :]), axis=2)  # [nv][8]
+    X = np.einsum("lv,cvd->cld", Nv, V[C])  # [cells][nv][3]
+    coords = np.empty((n, 3))
+    coords[cd.reshape(-1)] = X.reshape(-1, 3)
+    return coords
+
+
+def test_full_size_hex3_properties(torch):
+    """bench.py's hex3 mesh (64^3 jittered, rotated, library numbering) at full size: the
+    Neumann kernel, physical linears (interior rows vanish, Galerkin exactness on trilinear
+    cells), and symmetry with the variable coefficient (R5), in the launch configuration
+    bench.py times."""
+    from paper_1910_13247_b200 import HexOperator, hex_number_dofs
+
+    V, C = synth.hex_mesh((64, 64, 64), jitter=0.2, seed=0)
+    k = 3
+    cd, n, bnd = hex_number_dofs(C, k)
+    assert n == 193 ** 3
+    op = HexOperator(V, C, k, cd, n)  # Neumann, c = 1
+    one = torch.ones(n, dtype=torch.float64, device="cuda")
+    d = op.diagonal()
+    assert op.apply(one).abs().max().item() <= 1e-12 * d.abs().max().item()
+    coords = _support_coords(V, C, cd, n, k)
+    u = torch.from_numpy(coords @ np.array([0.3, -1.1, 0.7]) + 0.4).cuda()
+    y = op.apply(u).cpu().numpy()
+    interior = ~bnd
+    assert np.abs(y[interior]).max() <= 1e-11 * d.abs().max().item()
+    assert np.abs(y[bnd]).max() > 1e-6
+    op = HexOperator(V, C, k, cd, n, dirichlet=np.nonzero(bnd)[0], coeff="variable")
+    a = torch.from_numpy(seeded(n, 1)).cuda()
+    b = torch.from_numpy(seeded(n, 2)).cuda()
+    lhs, rhs = torch.dot(a, op.apply(b)).item(), torch.dot(b, op.apply(a)).item()
+    assert abs(lhs - rhs) <= 1e-12 * a.norm().item() * b.norm().item() * d.abs().max().item()
