@@ -76,3 +76,37 @@ def test_dg_chebyshev_pcg_matches_oracle(case, torch):
     if len(h) < 2 or min(h[-2] / (1e-10 * normb) - 1.0, 1.0 - h[-1] / (1e-10 * normb)) > 1e-6:
         assert res.iterations == ref.iterations
     assert rel_l2(x.cpu().numpy(), ref.x) <= 1e-8
+
+
+def test_full_size_dg4_sampled_cells(torch):
+    """bench.py's dg4 operator (Q4, 64^3 cells, 32.8 M DoFs) on a seeded vector, in the launch
+    configuration bench.py times; sampled cells (corners, faces, interior) checked against the
+    oracle on the clipped 3x3x3 sub-brick around each: a cell's rows involve only its six
+    neighbours, the local h and, on domain faces, the Nitsche terms, all of which the
+    sub-brick reproduces exactly."""
+    from paper_1910_13247_b200 import Operator
+
+    n, k = 64, 4
+    NV = (k + 1) ** 3
+    op = Operator((n, n, n), k, discretization="dg")
+    x = seeded(op.n_local, 5)
+    y = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    h = 1.0 / n
+    for cell in [(0, 0, 0), (63, 63, 63), (31, 17, 45), (0, 40, 12), (63, 5, 0), (20, 63, 33), (1, 1, 62)]:
+        lo = [max(0, c - 1) for c in cell]
+        hi = [min(n - 1, c + 1) for c in cell]
+        ns = [b - a + 1 for a, b in zip(lo, hi)]
+        S = dg.assemble(tuple(ns), k, lower=tuple(a * h for a in lo), upper=tuple((b + 1) * h for b in hi))
+        xs = np.empty(S.shape[0])
+        for cz in range(ns[2]):
+            for cy in range(ns[1]):
+                for cx in range(ns[0]):
+                    s = (cz * ns[1] + cy) * ns[0] + cx
+                    g = ((lo[2] + cz) * n + lo[1] + cy) * n + lo[0] + cx
+                    xs[s * NV:(s + 1) * NV] = x[g * NV:(g + 1) * NV]
+        ys = S @ xs
+        t = [c - a for c, a in zip(cell, lo)]
+        s = (t[2] * ns[1] + t[1]) * ns[0] + t[0]
+        g = (cell[2] * n + cell[1]) * n + cell[0]
+        ref = ys[s * NV:(s + 1) * NV]
+        assert np.abs(y[g * NV:(g + 1) * NV] - ref).max() <= 1e-12 * np.abs(ref).max(), cell
