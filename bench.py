@@ -240,11 +240,16 @@ def run_reference(args, cfg):
     el = time.perf_counter() - t0
     v = n * args.steps / el
     sample = f"oracle CSR SpMV (assembled by full Gauss quadrature) of the same Q{k} operator on a {cells}^3 sub-{'mesh' if geom == 'hex' else 'brick'} ({n} DoFs), one SpMV per step"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    ncw = (nc[0], nc[1], nc[2] * world)
+    n_full = (ncw[0] * ncw[1] * ncw[2] * (k + 1) ** 3 if geom == "dg"
+              else (k * ncw[0] + 1) * (k * ncw[1] + 1) * (k * ncw[2] + 1))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "DoFs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "sample": sample},
+        "config": {"workload": desc, "config": cfg, "n_cells": list(ncw), "degree": k, "n_dofs": n_full,
+                   "geometry": geom, "coeff": coeff, "parallelism": f"zslab{world}", "sample": sample},
         "cpu_baseline": {"value": v, "unit": "DoFs/s", "cores": oracle.num_threads(), "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "DoFs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
