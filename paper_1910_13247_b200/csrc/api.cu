@@ -603,8 +603,9 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
   const char *pe = std::getenv("MF_HOST_PIPELINE");
   const int C = (pe && std::atoi(pe) > 0) ? std::atoi(pe) : 8;
   const int var = chosen_variant(op);
-  const bool pipelined = !op->dg && op->world == 1 && g.dim == 3 &&
-                         (var == kVariantCartPlane || var == kVariantGeneral) && C > 1 && g.nc[2] >= 2 * C;
+  const bool pipelined = !op->hex && op->world == 1 && g.dim == 3 &&
+                         (var == kVariantCartPlane || var == kVariantGeneral || var == kVariantDG) && C > 1 &&
+                         g.nc[2] >= 2 * C;
   if (!pipelined) {
     CUDA_TRY(cudaMemcpyAsync(op->h_src, src_host, bytes, cudaMemcpyHostToDevice, op->stream));
     STATUS_TRY(apply_impl(op, op->h_src, op->h_dst));
@@ -631,6 +632,30 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
   // the previous call's work on the op's stream is done before its buffers are reused
   CUDA_TRY(cudaEventRecord(op->ev_out[C - 1], op->stream));
   CUDA_TRY(cudaStreamWaitEvent(op->h2d_s, op->ev_out[C - 1], 0));
+  if (var == kVariantDG) {
+    // DG: cell-major DoFs, a cell layer is one contiguous run of L DoFs; range r computes
+    // layers [z0, z1) and needs layer z1 for the z-couplings of its top layer
+    const int64_t layer = g.nc[0] * g.nc[1], L = layer * ipow(K + 1, 3);
+    int64_t up = 0;  // layers uploaded so far
+    for (int r = 0; r < C; ++r) {
+      const int64_t z0 = nz * r / C, z1 = nz * (r + 1) / C, need = std::min(z1 + 1, nz);
+      if (need > up) {
+        CUDA_TRY(cudaMemcpyAsync(op->h_src + up * L, src_host + up * L, (need - up) * L * sizeof(double),
+                                 cudaMemcpyHostToDevice, op->h2d_s));
+        up = need;
+      }
+      CUDA_TRY(cudaEventRecord(op->ev_in[r], op->h2d_s));
+      CUDA_TRY(cudaStreamWaitEvent(op->stream, op->ev_in[r], 0));
+      CUDA_TRY(launch_apply_dg(g, op->t, op->h_src, op->h_dst, op->stream, &op->launches, z0 * layer, z1 * layer));
+      CUDA_TRY(cudaEventRecord(op->ev_out[r], op->stream));
+      CUDA_TRY(cudaStreamWaitEvent(op->d2h_s, op->ev_out[r], 0));
+      CUDA_TRY(cudaMemcpyAsync(dst_host + z0 * L, op->h_dst + z0 * L, (z1 - z0) * L * sizeof(double),
+                               cudaMemcpyDeviceToHost, op->d2h_s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(op->d2h_s));
+    CUDA_TRY(cudaStreamSynchronize(op->stream));
+    return MF_OK;
+  }
   for (int r = 0; r < C; ++r) {
     const int64_t z0 = nz * r / C, z1 = nz * (r + 1) / C;
     const int64_t in0 = r == 0 ? 0 : K * z0 + 1, in1 = K * z1;  // node planes, inclusive

@@ -90,8 +90,9 @@ cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float 
                                      const float *metric, cudaStream_t s, int64_t *launches);
 bool cart_plane_supported(const Geo &g);
 // DG-SIP operator and its diagonal (kernels_dg.cu, §8(f) f4)
+// cells [cbeg, cend) only (cend < 0: every cell); DoFs cell-major, plain stores
 cudaError_t launch_apply_dg(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
-                            int64_t *launches);
+                            int64_t *launches, int64_t cbeg = 0, int64_t cend = -1);
 cudaError_t launch_diagonal_dg(const Geo &g, const Tables &t, double *diag, cudaStream_t s, int64_t *launches);
 cudaError_t launch_metric(const Geo &g, const Tables &t, double *metric, int *bad, cudaStream_t s,
                           int64_t *launches);

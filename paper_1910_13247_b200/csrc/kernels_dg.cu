@@ -71,17 +71,18 @@ __device__ __forceinline__ int slot(int e, int p, int i) {
 
 template <int K>
 __global__ void __launch_bounds__(256) k_apply_dg(const __grid_constant__ DGParams D, const double *__restrict__ src,
-                                                  double *__restrict__ dst, int cpb) {
+                                                  double *__restrict__ dst, int cpb, int64_t cbeg,
+                                                  int64_t cend) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   extern __shared__ double sm[];
   const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
   const bool active = cl < cpb;
-  const int64_t cell = (int64_t)blockIdx.x * cpb + cl;
-  const bool valid = active && cell < ncells;
+  const int64_t cell = cbeg + (int64_t)blockIdx.x * cpb + cl;  // cells [cbeg, cend)
+  const bool valid = active && cell < cend;
   // shared memory: the contiguous cells [cell0 - 1, cell0 + cpb] (own cells and their
   // x-neighbours, one coalesced load), then T and W per cell
-  const int64_t cell0 = (int64_t)blockIdx.x * cpb;
+  const int64_t cell0 = cbeg + (int64_t)blockIdx.x * cpb;
   double *Ux = sm, *U = Ux + (cl + 1) * NV;
   double *T = sm + (cpb + 2) * NV + (active ? cl : 0) * 2 * NV, *W = T + NV;
   int64_t c[3] = {0, 0, 0};
@@ -189,13 +190,13 @@ __device__ __forceinline__ void self_bnd(const double (&bl)[kMaxN], const double
 // products, two barriers, and 2 (k+1)^3 + 12 (k+1)^2 doubles of shared memory per cell.
 template <int K>
 __global__ void __launch_bounds__(256) k_apply_dg2(const __grid_constant__ DGParams D, const double *__restrict__ src,
-                                                   double *__restrict__ dst, int cpb) {
+                                                   double *__restrict__ dst, int cpb, int64_t cbeg,
+                                                   int64_t cend) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N, CS = 2 * NV + 12 * NP;
   extern __shared__ double sm[];
-  const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
-  const int64_t cell = (int64_t)blockIdx.x * cpb + cl;
-  const bool valid = cl < cpb && cell < ncells;
+  const int64_t cell = cbeg + (int64_t)blockIdx.x * cpb + cl;  // cells [cbeg, cend)
+  const bool valid = cl < cpb && cell < cend;
   // the y / z masses, read by thread-dependent rows in the trace transforms: shared
   // memory (a per-thread row of the parameter bank would serialise on the constant cache)
   double *My = sm + cpb * CS, *Mz = My + NP;
@@ -492,7 +493,8 @@ double dg_rank2_defect(const DGParams &D, int N) {
 }
 
 template <int K>
-cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaStream_t s) {
+cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaStream_t s, int64_t cbeg,
+                        int64_t cend) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   static const bool v1 = std::getenv("MF_DG_V1") != nullptr;
   if (!v1 && dg_rank2_defect(D, N) <= 1e-14) {
@@ -503,9 +505,10 @@ cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaS
                          true);
     (void)attr2;
     const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
-    const int64_t blocks = (ncells + cpb - 1) / cpb;
-    if (blocks == 0) return cudaSuccess;
-    k_apply_dg2<K><<<(unsigned)blocks, ((cpb * NP + 31) / 32) * 32, smem, s>>>(D, src, dst, cpb);
+    (void)ncells;
+    const int64_t blocks = (cend - cbeg + cpb - 1) / cpb;
+    if (blocks <= 0) return cudaSuccess;
+    k_apply_dg2<K><<<(unsigned)blocks, ((cpb * NP + 31) / 32) * 32, smem, s>>>(D, src, dst, cpb, cbeg, cend);
     return cudaGetLastError();
   }
   int cpb = 256 / NP;
@@ -516,28 +519,30 @@ cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaS
                       true);
   (void)attr;
   const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
-  const int64_t blocks = (ncells + cpb - 1) / cpb;
-  if (blocks == 0) return cudaSuccess;
-  k_apply_dg<K><<<(unsigned)blocks, ((cpb * NP + 31) / 32) * 32, smem, s>>>(D, src, dst, cpb);
+  (void)ncells;
+  const int64_t blocks = (cend - cbeg + cpb - 1) / cpb;
+  if (blocks <= 0) return cudaSuccess;
+  k_apply_dg<K><<<(unsigned)blocks, ((cpb * NP + 31) / 32) * 32, smem, s>>>(D, src, dst, cpb, cbeg, cend);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_apply_dg(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
-                            int64_t *launches) {
+                            int64_t *launches, int64_t cbeg, int64_t cend) {
   DGParams D;
   build_dg(g, t, &D);
   ++*launches;
+  if (cend < 0) cend = g.nc[0] * g.nc[1] * g.nc[2];
   switch (g.k) {
-    case 1: return launch_dg_t<1>(D, src, dst, s);
-    case 2: return launch_dg_t<2>(D, src, dst, s);
-    case 3: return launch_dg_t<3>(D, src, dst, s);
-    case 4: return launch_dg_t<4>(D, src, dst, s);
-    case 5: return launch_dg_t<5>(D, src, dst, s);
-    case 6: return launch_dg_t<6>(D, src, dst, s);
-    case 7: return launch_dg_t<7>(D, src, dst, s);
-    case 8: return launch_dg_t<8>(D, src, dst, s);
+    case 1: return launch_dg_t<1>(D, src, dst, s, cbeg, cend);
+    case 2: return launch_dg_t<2>(D, src, dst, s, cbeg, cend);
+    case 3: return launch_dg_t<3>(D, src, dst, s, cbeg, cend);
+    case 4: return launch_dg_t<4>(D, src, dst, s, cbeg, cend);
+    case 5: return launch_dg_t<5>(D, src, dst, s, cbeg, cend);
+    case 6: return launch_dg_t<6>(D, src, dst, s, cbeg, cend);
+    case 7: return launch_dg_t<7>(D, src, dst, s, cbeg, cend);
+    case 8: return launch_dg_t<8>(D, src, dst, s, cbeg, cend);
   }
   return cudaErrorInvalidValue;
 }
