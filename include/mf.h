@@ -204,6 +204,8 @@ typedef struct {
   double cheb_range;     /* 20 */
   double cheb_safety;    /* 1.2 */
   int32_t eig_cg_steps;  /* 12 */
+  int32_t precision;     /* 0: FP64 Chebyshev; 1: the Chebyshev preconditioner in FP32 inside the FP64 CG
+                            (§8(f) f2; 3D brick, one rank, else MF_ERR_ARGUMENT) */
 } mf_cg_params;
 
 typedef struct {

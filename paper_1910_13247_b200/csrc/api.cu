@@ -31,6 +31,7 @@ struct mf_op {
   double *r = nullptr, *p = nullptr, *v = nullptr, *z = nullptr, *cd = nullptr, *cax = nullptr;
   // FP32 copies / scratch for the mixed-precision multigrid (lazily allocated)
   float *metric_f = nullptr, *dinv_f = nullptr, *cd_f = nullptr, *cax_f = nullptr;
+  float *r_f = nullptr, *z_f = nullptr;  // mixed-precision Chebyshev-PCG (mf_cg_params.precision = 1)
   double *partials = nullptr, *dev_scal = nullptr, *host_scal = nullptr;
   double *h_src = nullptr, *h_dst = nullptr;  // device buffers for mf_apply_host
   double *recv_lo = nullptr, *recv_hi = nullptr;
@@ -247,7 +248,7 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
 extern "C" void mf_destroy(mf_op *op) {
   if (!op) return;
   cudaFree(op->metric);
-  for (float *b : {op->metric_f, op->dinv_f, op->cd_f, op->cax_f}) cudaFree(b);
+  for (float *b : {op->metric_f, op->dinv_f, op->cd_f, op->cax_f, op->r_f, op->z_f}) cudaFree(b);
   for (double *b : {op->diag, op->dinv, op->r, op->p, op->v, op->z, op->cd, op->cax, op->partials, op->dev_scal,
                     op->h_src, op->h_dst, op->recv_lo, op->recv_hi})
     cudaFree(b);
@@ -968,7 +969,23 @@ extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t 
     lam *= prm->cheb_safety;
     res->lambda_max = lam;
   }
+  if (prm->precision != 0 && prm->precision != 1) return fail(MF_ERR_ARGUMENT, "precision must be 0 or 1");
+  const bool mixed = prm->precision == 1 && prm->cheb_degree > 0;
+  if (mixed) {
+    if (op->world != 1 || op->g.dim != 3 || op->dg || op->hex)
+      return fail(MF_ERR_ARGUMENT, "FP32 Chebyshev: 3D brick operator, one rank");
+    if (!op->r_f) {
+      CUDA_TRY(cudaMalloc(&op->r_f, n * sizeof(float)));
+      CUDA_TRY(cudaMalloc(&op->z_f, n * sizeof(float)));
+    }
+  }
   auto precond = [&](const double *rr, double *zz) -> mf_status {
+    if (mixed) {  // z = P(r) in FP32: round r, run the same Chebyshev recurrence, widen z
+      CUDA_TRY(launch_d2f(rr, op->r_f, n, op->stream, &op->launches));
+      STATUS_TRY(cheb_f32(op, op->r_f, op->z_f, lam, prm->cheb_degree, prm->cheb_range));
+      CUDA_TRY(launch_f2d(op->z_f, zz, n, op->stream, &op->launches));
+      return MF_OK;
+    }
     if (prm->cheb_degree > 0) return cheb_impl(op, rr, zz, lam, prm->cheb_degree, prm->cheb_range);
     CUDA_TRY(launch_mul(op->dinv, rr, zz, n, op->stream, &op->launches));
     return MF_OK;

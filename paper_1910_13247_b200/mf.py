@@ -46,7 +46,8 @@ class Dist(ctypes.Structure):
 
 class CGParams(ctypes.Structure):
     _fields_ = [("rel_tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("cheb_degree", ctypes.c_int32),
-                ("cheb_range", ctypes.c_double), ("cheb_safety", ctypes.c_double), ("eig_cg_steps", ctypes.c_int32)]
+                ("cheb_range", ctypes.c_double), ("cheb_safety", ctypes.c_double), ("eig_cg_steps", ctypes.c_int32),
+                ("precision", ctypes.c_int32)]
 
 
 class CGResultC(ctypes.Structure):
@@ -328,9 +329,11 @@ class Operator:
         return out
 
     def cg_solve(self, b, x=None, rel_tol=1e-10, max_iter=10000, cheb_degree=6, cheb_range=20.0,
-                 cheb_safety=1.2, eig_cg_steps=12, history_cap=20000):
+                 cheb_safety=1.2, eig_cg_steps=12, history_cap=20000, precision="fp64"):
+        """Chebyshev-Jacobi PCG; precision="mixed" runs the Chebyshev preconditioner in FP32."""
         x = self.new_vector() if x is None else x
-        p = CGParams(rel_tol, max_iter, cheb_degree, cheb_range, cheb_safety, eig_cg_steps)
+        p = CGParams(rel_tol, max_iter, cheb_degree, cheb_range, cheb_safety, eig_cg_steps,
+                     {"fp64": 0, "mixed": 1}[precision])
         r = CGResultC()
         hist = np.zeros(history_cap)
         self._stream()

@@ -137,3 +137,21 @@ def test_cg_errors(torch):
     assert e.value.name == "MF_ERR_MAX_ITERATIONS"
     x, res = cuda_operator(case).cg_solve(torch.zeros_like(b))
     assert res.iterations == 0 and x.abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("case", [dict(dim=3, n_cells=(16, 16, 16), k=2), dict(dim=3, n_cells=(8, 8, 8), k=4),
+                                  dict(dim=3, n_cells=(8, 8, 8), k=3, geometry="sine", coeff="variable")],
+                         ids=lambda c: f"k{c['k']}-{c.get('geometry', 'cart')}")
+def test_mixed_precision_chebyshev_pcg(case, torch):
+    # §8(f) f2 on the a10 path: the Chebyshev(6) preconditioner in FP32 inside the FP64 CG
+    # (the preconditioner changes by O(1e-7), CG keeps the FP64 residual recursion): the
+    # FP64 stopping test is met, in at most two more iterations than the FP64 oracle run
+    p, A, d, s = _oracle_setup(case)
+    b = oracle.rhs(p, 0)
+    ref = solvers.chebyshev_pcg(A.matvec, d, b, s, rel_tol=1e-10)
+    op = cuda_operator(case)
+    x, res = op.cg_solve(torch.from_numpy(b).cuda(), rel_tol=1e-10, precision="mixed")
+    assert res.final_rel_residual <= 1e-10
+    assert ref.iterations - 1 <= res.iterations <= ref.iterations + 2, (res.iterations, ref.iterations)
+    assert rel_l2(x.cpu().numpy(), ref.x) <= 1e-8
+    assert abs(res.lambda_max - ref.lambda_max) <= 1e-9 * ref.lambda_max
