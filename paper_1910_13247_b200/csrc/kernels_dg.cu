@@ -192,19 +192,23 @@ template <int K>
 __global__ void __launch_bounds__(256) k_apply_dg2(const __grid_constant__ DGParams D, const double *__restrict__ src,
                                                    double *__restrict__ dst, int cpb, int64_t cbeg,
                                                    int64_t cend) {
-  constexpr int N = K + 1, NP = N * N, NV = NP * N, CS = 2 * NV + 12 * NP;
+  // shared memory: per cell W/C and Z/E (stride CW = 2 NV + 3 doubles: an odd stride spreads
+  // the y-pencil accesses of neighbouring cells over the banks), then per cell the trace pairs
+  // (16-byte aligned), then the y / z masses
+  constexpr int N = K + 1, NP = N * N, NV = NP * N, CW = 2 * NV + 3, CT = 12 * NP;
   extern __shared__ double sm[];
   const int cl = threadIdx.x / NP, p = threadIdx.x - cl * NP;
   const int64_t cell = cbeg + (int64_t)blockIdx.x * cpb + cl;  // cells [cbeg, cend)
   const bool valid = cl < cpb && cell < cend;
   // the y / z masses, read by thread-dependent rows in the trace transforms: shared
   // memory (a per-thread row of the parameter bank would serialise on the constant cache)
-  double *My = sm + cpb * CS, *Mz = My + NP;
+  const int tr0 = (cpb * CW + 1) & ~1;
+  double *My = sm + tr0 + cpb * CT, *Mz = My + NP;
   for (int i = threadIdx.x; i < 2 * NP; i += blockDim.x) My[i] = D.M[1 + i / NP][(i % NP) / N][i % N];
-  double *WC = sm + (valid ? cl : 0) * CS, *ZE = WC + NV;
+  double *WC = sm + (valid ? cl : 0) * CW, *ZE = WC + NV;
   // neighbour traces as (a . u_nb, u_nb[face]) pairs: TR[face][NP], face = y-lo, y-hi, x-lo,
   // x-hi; T1[2][NP] the x-face pairs after M_z
-  double2 *TR = reinterpret_cast<double2 *>(ZE + NV), *T1 = TR + 4 * NP;
+  double2 *TR = reinterpret_cast<double2 *>(sm + tr0 + (valid ? cl : 0) * CT), *T1 = TR + 4 * NP;
   int64_t c[3] = {0, 0, 0};
   if (valid) {
     c[0] = cell % D.nc[0];
@@ -498,9 +502,9 @@ cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaS
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
   static const bool v1 = std::getenv("MF_DG_V1") != nullptr;
   if (!v1 && dg_rank2_defect(D, N) <= 1e-14) {
-    constexpr int CS = 2 * NV + 12 * NP;
+    constexpr int CW = 2 * NV + 3, CT = 12 * NP;
     const int cpb = 256 / NP;
-    const size_t smem = (size_t)(cpb * CS + 2 * NP) * sizeof(double);
+    const size_t smem = (size_t)(((cpb * CW + 1) & ~1) + cpb * CT + 2 * NP) * sizeof(double);
     static bool attr2 = (cudaFuncSetAttribute(k_apply_dg2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                          true);
     (void)attr2;
