@@ -40,7 +40,12 @@ struct PlaneShape {
   static constexpr int NT = NCELL * K;          // face phase: (cell, p = 1..K); column phase: (cell, j)
   static_assert(NT % 32 == 0, "tile must give whole warps");
   static_assert(NXc + NYc - 1 <= NT, "one edge column per thread");
-  static constexpr int SPL = NCOL | 1;          // stage plane pitch
+  // stage layout: node x of a row sits at XS(x) = x + x / 16 (a pad double every 16 nodes), the
+  // row pitch is NXp and the plane pitch SPL = 2 (mod 16): the face phase's warp (8 cells 4
+  // nodes apart x 4 planes) then hits 16 distinct bank pairs per half-warp (FP64)
+  static constexpr int XS(int x) { return x + (x >> 4); }
+  static constexpr int NXp = XS(NXc - 1) + 1;
+  static constexpr int SPL = NXp * NYc + ((2 - (NXp * NYc) % 16) + 16) % 16;  // stage plane pitch
   static constexpr int STG = N * SPL;           // u on planes 0..K of a layer
   static constexpr int FACE = N * N;
   static constexpr int NV = NCELL * N * FACE;   // P (or Q): faces of planes 0..K
@@ -52,7 +57,7 @@ template <int K, int TX, int TY, bool ISO, class T>
 __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 : 3)
     k_apply_plane(const __grid_constant__ TileParams P, const T *__restrict__ src, T *__restrict__ dst) {
   using S = PlaneShape<K, TX, TY>;
-  constexpr int N = S::N, NXc = S::NXc, NCELL = S::NCELL, SPL = S::SPL, FACE = S::FACE;
+  constexpr int N = S::N, NXp = S::NXp, NCELL = S::NCELL, SPL = S::SPL, FACE = S::FACE;
   constexpr int h = (N + 1) / 2;
   constexpr int PSTRIDE = TX * FACE;       // face slot of (cx, cy, p) = cx + TX (p + N cy)
   constexpr int YSTRIDE = TX * N * FACE;   // cy -> cy + 1
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
     const bool has_e = edge_xy(I, ex, ey);
     const bool e_ok = has_e && !xy_cons(I, ex, ey);
     const T *go = sp0 + y * Nx + K * ccx, *ge = sp0 + ey * Nx + ex;
-    T *so = Us + y * NXc + K * ccx, *se = Us + ey * NXc + ex;
+    T *so = Us + y * NXp, *se = Us + ey * NXp + S::XS(ex);
 #pragma unroll
     for (int l = 0; l <= K; ++l) {
       if (l >= l0) {
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             const bool ok = !zc && !ycons && !(i == 0 && xcons0);
-            cp_async_z<T>(so + l * SPL + i, go + i, ok ? 8u : 0u);
+            cp_async_z<T>(so + l * SPL + S::XS(K * ccx + i), go + i, ok ? 8u : 0u);
           }
         }
         if (has_e) cp_async_z<T>(se + l * SPL, ge, (e_ok && !zc) ? 8u : 0u);
@@ -147,14 +152,14 @@ __global__ void __launch_bounds__(PlaneShape<K, TX, TY>::NT, sizeof(T) == 8 ? 2 
 
   // ---- face: P and Q on the face of cell (fcx, fcy) at plane p from u on that plane
   auto face = [&](int p) {
-    const T *Ul = Us + p * SPL + (K * fcy) * NXc + K * fcx;
+    const T *Ul = Us + p * SPL + (K * fcy) * NXp;
     T *Pf = Vp + (fcx + TX * (p + N * fcy)) * FACE, *Qf = Vq + (fcx + TX * (p + N * fcy)) * FACE;
     T c[N][N], g[N][N];  // [j][i]: c = M_y u, g = Ky' u
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       T uv[N], e[h], o[h], ve[h], vo[h], t[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) uv[j] = Ul[j * NXc + i];
+      for (int j = 0; j < N; ++j) uv[j] = Ul[j * NXp + S::XS(K * fcx + i)];
       eo_split<N>(uv, e, o);
       eo_first<N>(Mm, e, o, ve, vo);
       eo_combine<N>(ve, vo, t);
