@@ -8,9 +8,12 @@ this module is a ctypes binding plus the solver algorithms of SURVEY.md
 §8(c) O9-O11 written out in numpy (``solvers.py``).
 
 Parity status: every routine is pinned by a
-``-m "not gpu"`` test against closed forms / exact integration / brute force,
-except the variable-coefficient operator on the deformed mesh, whose parity is
-"parity unpinned" beyond invariants (Neumann kernel, symmetry, linears).
+``-m "not gpu"`` test against closed forms / exact integration / brute force.
+The variable-coefficient operator on the deformed mesh has no closed form; it
+is pinned by invariants (Neumann kernel, symmetry, linears) and by the energy
+of the physical linears, u_a^T A u_b = delta_ab int c dx, against a mesh-free
+quadrature of int c (tests/test_oracle_operator.py::
+test_deformed_variable_coefficient_energy_of_linears).
 """
 from __future__ import annotations
 

@@ -7,10 +7,11 @@
  * line numbers; readings R1-R15 are listed in DESIGN.md).
  *
  * Parity pins for each routine live in tests/test_oracle_*.py (closed forms,
- * exact polynomial integration, invariants, brute force).  The one function
- * with no closed-form pin beyond invariants is the variable-coefficient
- * operator on the deformed mesh: "parity unpinned" except for the Neumann
- * kernel, symmetry and agreement between or_assemble_csr / or_apply_rows.
+ * exact polynomial integration, invariants, brute force).  The variable-
+ * coefficient operator on the deformed mesh has no closed form; it is pinned
+ * by the Neumann kernel, symmetry, or_assemble_csr = or_apply_rows, and the
+ * energy of the physical linears (u_a^T A u_b = delta_ab int c dx against a
+ * mesh-free quadrature of int c; tests/test_oracle_operator.py).
  */
 #include "oracle.h"
 

@@ -258,6 +258,24 @@ def test_cfg4_full_size_sampled_rows(torch):
     assert np.abs(y[rows] - ref).max() <= CUDA_ORACLE_TOL * np.abs(ref).max()
 
 
+def test_cfg4_full_size_energy_of_linears(torch):
+    # BASELINE configs[3] geometry and coefficient (Q3, deformed 64^3, variable c) under Neumann:
+    # u_a^T A u_b = delta_ab int c dx for the physical linears u_a = x_a (the property
+    # tests/test_oracle_operator.py::test_deformed_variable_coefficient_energy_of_linears pins
+    # on the oracle), checked at full size where the oracle cannot assemble
+    from tests.test_oracle_operator import _integral_of_c_unit_cube, _node_coords
+
+    case = dict(dim=3, n_cells=(64, 64, 64), k=3, geometry="sine", coeff="variable", dirichlet=0)
+    p = oracle_problem(case)
+    op = cuda_operator(case)
+    X = torch.from_numpy(_node_coords(p, physical=True)).cuda()
+    AX = [op.apply(X[:, b].contiguous()) for b in range(3)]
+    G = np.array([[torch.dot(X[:, a], AX[b]).item() for b in range(3)] for a in range(3)])
+    Ic = _integral_of_c_unit_cube()
+    assert np.abs(G - G[0, 0] * np.eye(3)).max() <= 1e-11 * Ic
+    assert abs(G[0, 0] - Ic) <= 1e-7 * Ic
+
+
 def _one_d(k, n, which):
     # global 1D stiffness (which=0) / mass (which=1) on [0,1] from the oracle, no constraints
     return oracle.CSR(oracle.problem(dim=1, n_cells=(n,), degree=k), which=which, dirichlet=False).dense()

@@ -171,6 +171,18 @@ def test_full_size_hex3_properties(torch):
     interior = ~bnd
     assert np.abs(y[interior]).max() <= 1e-11 * d.abs().max().item()
     assert np.abs(y[bnd]).max() > 1e-6
+    # variable coefficient under Neumann: u_a^T A u_b = delta_ab int c dx for the physical
+    # linears (pinned on the oracle by test_oracle_hex.py::
+    # test_variable_coefficient_energy_of_linears_on_jittered_mesh)
+    from tests.test_oracle_operator import _integral_of_c_unit_cube
+
+    op = HexOperator(V, C, k, cd, n, coeff="variable")
+    X = torch.from_numpy(coords).cuda()
+    AX = [op.apply(X[:, j].contiguous()) for j in range(3)]
+    G = np.array([[torch.dot(X[:, i], AX[j]).item() for j in range(3)] for i in range(3)])
+    Ic = _integral_of_c_unit_cube()
+    assert np.abs(G - G[0, 0] * np.eye(3)).max() <= 1e-11 * Ic
+    assert abs(G[0, 0] - Ic) <= 1e-6 * Ic
     op = HexOperator(V, C, k, cd, n, dirichlet=np.nonzero(bnd)[0], coeff="variable")
     a = torch.from_numpy(seeded(n, 1)).cuda()
     b = torch.from_numpy(seeded(n, 2)).cuda()

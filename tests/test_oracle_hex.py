@@ -68,6 +68,27 @@ def test_linears_on_jittered_mesh(k):
     assert np.linalg.eigvalsh(Ad).min() > 0
 
 
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_variable_coefficient_energy_of_linears_on_jittered_mesh(k):
+    # u_a^T A u_b = delta_ab int c dx for the physical linears u_a = x_a under Neumann (the
+    # jitter moves interior vertices only, so the mesh covers the unit cube exactly): G is a
+    # multiple of the identity to rounding, its diagonal converges to the mesh-free integral
+    # of c (tests/test_oracle_operator.py::_integral_of_c_unit_cube)
+    from tests.test_oracle_operator import _integral_of_c_unit_cube
+
+    Ic = _integral_of_c_unit_cube()
+    errs = []
+    for n in (2, 6):
+        m = hm.conforming((n, n, n), k, jitter=0.25, seed=11 + k)
+        A = hm.oracle_matrix(m, coeff="variable", dirichlet=False)
+        X = m["coords"]
+        G = np.array([[X[:, a] @ (A @ X[:, b]) for b in range(3)] for a in range(3)])
+        assert np.abs(G - G[0, 0] * np.eye(3)).max() <= 1e-13 * Ic
+        errs.append(abs(G[0, 0] - Ic) / Ic)
+    assert errs[1] <= errs[0] / 9  # converging (at least h^2 over a 3x refinement)
+    assert errs[1] <= {1: 3e-4, 2: 3e-5, 3: 2e-6}[k]  # measured 1.6e-4, 1.3e-5, 6.3e-7
+
+
 @pytest.mark.parametrize("k", [2, 3])
 def test_quadratics_on_sheared_mesh(k):
     m = hm.conforming((2, 2, 2), k, jitter=0.0, seed=3)

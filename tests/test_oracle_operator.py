@@ -195,6 +195,48 @@ def test_deformed_linears_reproduced(k):
     assert np.abs(r[inner]).max() <= 1e-13 * np.abs(A.val).max() * np.abs(u).max()
 
 
+def _integral_of_c_unit_cube(m=8, q=16):
+    """int_[0,1]^3 c(x) dx for R5's c(x) = 1/(0.05 + 2|x|^2), by a tensor Gauss rule on m^3
+    sub-boxes (numpy leggauss) -- no mesh, no mapping, nothing from the oracle; converged to
+    1e-16 at (8, 16) (equal to the (4, 16) and (12, 16) rules)."""
+    from numpy.polynomial.legendre import leggauss
+
+    x, w = leggauss(q)
+    pts = (np.arange(m)[:, None] + (x[None, :] + 1) / 2).ravel() / m
+    ws = np.tile(w / 2, m) / m
+    X, Y, Z = np.meshgrid(pts, pts, pts, indexing="ij", sparse=True)
+    W = ws[:, None, None] * ws[None, :, None] * ws[None, None, :]
+    return float((W / (0.05 + 2 * (X * X + Y * Y + Z * Z))).sum())
+
+
+# |G00 - int c| / int c at n = 8 cells per direction, with margin over the measured
+# quadrature errors 1.9e-5, 1.6e-6, 7.6e-8, 2.0e-9 (k = 1..4)
+_ENERGY_TOL_N8 = {1: 1e-4, 2: 1e-5, 3: 1e-6, 4: 2e-8}
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_deformed_variable_coefficient_energy_of_linears(k):
+    # Pins the curved, variable-coefficient operator (R4, R5) beyond its invariants.  A physical
+    # linear u_a = x_a lies in the isoparametric space, its gradient is e_a, so
+    #   u_a^T A u_b = int c grad(x_a) . grad(x_b) dx = delta_ab int c dx   (Neumann, P:271-283).
+    # The discrete sum sum_q c(x_q) w_q |det J_q| (J^-T J^T e_a).(J^-T J^T e_b) is delta_ab times
+    # ONE quadrature of int c, so G = [u_a^T A u_b] must be a multiple of the identity to
+    # rounding (a transposed J^-1 J^-T, a wrong metric entry or a missing symmetric term breaks
+    # that), and its diagonal must converge to the mesh-free integral of c (a missing |det J|,
+    # c at the reference point instead of x_q, or a wrong Gauss weight breaks that).
+    Ic = _integral_of_c_unit_cube()
+    errs = []
+    for n in (2, 8):
+        p = oracle.problem(dim=3, n_cells=(n, n, n), degree=k, geom=1, eps=0.1, coeff_kind=1, dirichlet=0)
+        A = oracle.CSR(p, dirichlet=False)
+        X = _node_coords(p, physical=True)
+        G = np.array([[X[:, a] @ (A @ X[:, b]) for b in range(3)] for a in range(3)])
+        assert np.abs(G - G[0, 0] * np.eye(3)).max() <= 1e-13 * Ic
+        errs.append(abs(G[0, 0] - Ic) / Ic)
+    assert errs[1] <= _ENERGY_TOL_N8[k]
+    assert errs[1] <= errs[0] / 16  # converging (at least h^2 over a 4x refinement)
+
+
 def test_deformed_jacobian_positive():
     p = oracle.problem(dim=3, n_cells=(2, 2, 2), degree=3, geom=1, eps=0.1)
     for c in range(8):
