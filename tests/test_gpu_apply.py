@@ -38,6 +38,11 @@ CASES = [
     dict(dim=3, n_cells=(8, 8, 8), k=3, geometry="sine", coeff="variable"),  # cfg 4 shape, small
     dict(dim=3, n_cells=(3, 3, 3), k=4, geometry="sine", coeff="variable", dirichlet=0),
     dict(dim=3, n_cells=(16, 16, 16), k=2),  # cfg 2
+    # degenerate meshes: every DoF constrained (A = I), one cell, one-cell-thick plates
+    dict(dim=3, n_cells=(1, 1, 1), k=1),
+    dict(dim=2, n_cells=(1, 1), k=3, dirichlet=0),
+    dict(dim=3, n_cells=(1, 6, 1), k=2, dirichlet=0),
+    dict(dim=3, n_cells=(1, 1, 5), k=3, geometry="sine", coeff="variable", dirichlet=0b110000),
 ]
 
 
@@ -79,6 +84,8 @@ TILE_CASES = [
     dict(dim=3, n_cells=(4, 8, 5), k=4, dirichlet=0b011001),
     dict(dim=3, n_cells=(1, 1, 1), k=4),
     dict(dim=3, n_cells=(5, 3, 20), k=4, dirichlet=0),
+    dict(dim=3, n_cells=(17, 1, 1), k=2, dirichlet=0),           # one-cell-thick in y and z
+    dict(dim=3, n_cells=(1, 5, 9), k=3, dirichlet=0b000011),
 ]
 
 
