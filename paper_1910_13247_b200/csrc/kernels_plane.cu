@@ -27,6 +27,7 @@
 //                 carried from the previous layer, store the k finished planes.
 // Shared tile-edge / chunk-plane nodes: init kernel + FP64 atomics (tile_common.cuh).
 #include <cstdlib>
+#include <cstring>
 
 #include "tile_common.cuh"
 
@@ -432,6 +433,17 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T
 
 bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }
 
+// k = 4 tiles: 16 x 2 cells by default -- 3 instead of 7 strided x tile-edge planes in
+// the init on 64^3 (its y-edge planes are contiguous rows); cfg 3 168.0 vs 173.9 us per
+// apply.  MF_PLANE_TILE=8x4 selects the square-ish tile (comparisons).
+static bool wide_tiles() {
+  static const bool w = [] {
+    const char *e = std::getenv("MF_PLANE_TILE");
+    return !(e && std::strcmp(e, "8x4") == 0);
+  }();
+  return w;
+}
+
 template <class T>
 static cudaError_t launch_cart_plane_any(const Geo &g, const Tables &t, const T *src, T *dst, cudaStream_t s,
                                         int64_t *launches, int part, int zr_lo = 0, int zr_hi = 0) {
@@ -442,7 +454,9 @@ static cudaError_t launch_cart_plane_any(const Geo &g, const Tables &t, const T 
   switch (g.k) {
     case 2: MF_PLANE_LAUNCH(2, 8, 8);
     case 3: MF_PLANE_LAUNCH(3, 8, 4);
-    case 4: MF_PLANE_LAUNCH(4, 8, 4);
+    case 4:
+      if (wide_tiles()) MF_PLANE_LAUNCH(4, 16, 2);
+      MF_PLANE_LAUNCH(4, 8, 4);
   }
 #undef MF_PLANE_LAUNCH
   return cudaErrorNotSupported;
