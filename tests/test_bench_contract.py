@@ -1,0 +1,54 @@
+"""bench.py's driver contract on CPU: the reference arm (the oracle, timed on the host cores)
+prints one JSON line with the keys the driver reads, on rank 0 only; under torchrun
+(world 2) the other rank exits 0 without work or output.  The GPU arm is covered by the
+round-end bench itself (it needs a B200)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = {"impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"}
+
+
+def _lines(out):
+    return [json.loads(s) for s in out.splitlines() if s.startswith("{")]
+
+
+def test_reference_arm_single_rank():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "cfg2", "--steps", "2",
+                        "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    (d,) = _lines(r.stdout)
+    assert KEYS <= set(d)
+    assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["dtype"] == "f64"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # cfg2: Q2 on 16^3 cells, (2*16+1)^3 DoFs
+    assert d["config"]["n_dofs"] == 33 ** 3 and d["config"]["parallelism"] == "zslab1"
+
+
+def test_reference_arm_world2_rank0_only():
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--impl", "reference",
+                        "--gpus", "2", "--config", "cfg2", "--steps", "1", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr
+    lines = _lines(r.stdout)
+    assert len(lines) == 1, r.stdout  # rank 1 prints nothing
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    # weak scaling: the z extent (and the DoF count) grows with the world size
+    assert d["config"]["n_cells"] == [16, 16, 32] and d["config"]["n_dofs"] == 33 * 33 * 65
+    assert d["config"]["parallelism"] == "zslab2"
+
+
+@pytest.mark.parametrize("bad", [["--config", "nope"], ["--impl", "nope"]])
+def test_bench_rejects_unknown_arguments(bad):
+    r = subprocess.run([sys.executable, "bench.py", *bad], cwd=ROOT, capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0
