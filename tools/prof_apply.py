@@ -1,5 +1,5 @@
 """Small driver for ncu captures: build one operator and run a few applies.
-python tools/prof_apply.py [--config cfg3] [--variant auto] [--reps 5]"""
+python tools/prof_apply.py [--config cfg3] [--variant auto] [--reps 5] [--cells n]"""
 import argparse
 import os
 import sys
@@ -16,8 +16,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--variant", default="auto")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--cells", type=int, default=0, help="override: n^3 cells")
 a = ap.parse_args()
 nc, k, geom, coeff, _ = CONFIGS[a.config]
+if a.cells:
+    nc = (a.cells,) * 3
 if geom == "hex":
     from bench import make_hex_operator
 
