@@ -482,10 +482,28 @@ __device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool ok) {
 
 // cells per block of k_apply_cell3: ~256 threads, ~128 with the staged metric
 // (6 NV doubles per cell of extra shared memory), shared memory <= 48 KB
+// Cartesian constant-coefficient Q6 (N = 7) in FP64: padded work layout, slot 54 z + 7 y + x,
+// arrays of 378 doubles, cell stride 1137.  The plain layout (plane pitch 49 = 1 mod 16) puts
+// the y-sweep lanes of consecutive z-planes on the same bank pairs; a bank model of the three
+// sweeps gives 553 instead of 602 wavefronts per block
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr bool cell3_padded() {
+  return GEOM == 0 && K == 6 && sizeof(T) == 8;
+}
+// elements per work array and per cell of k_apply_cell3
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr int cell3_as() {
+  return cell3_padded<K, GEOM, T>() ? 54 * (K + 1) : (K + 1) * (K + 1) * (K + 1);
+}
+template <int K, int GEOM, class T>
+__host__ __device__ constexpr int cell3_cs() {
+  return cell3_padded<K, GEOM, T>() ? 3 * cell3_as<K, GEOM, T>() + 3 : 3 * (K + 1) * (K + 1) * (K + 1);
+}
+
 template <int K, int GEOM, class T = double>
 __host__ __device__ constexpr int cell3_cpb() {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
-  constexpr int per_cell = (int)sizeof(T) * (3 + (GEOM >= 2 ? 6 : 0)) * NV;
+  constexpr int per_cell = (int)sizeof(T) * (cell3_cs<K, GEOM, T>() + (GEOM >= 2 ? 6 * NV : 0));
   int c = (GEOM >= 2 ? 128 : 256) / NP;
   while (c > 1 && c * per_cell > 48 * 1024) --c;
   return c < 1 ? 1 : c;
@@ -494,7 +512,8 @@ __host__ __device__ constexpr int cell3_cpb() {
 template <int K, int GEOM, class T>
 __host__ __device__ constexpr int cell3_ms_off() {
   constexpr int NV = (K + 1) * (K + 1) * (K + 1), E = 16 / (int)sizeof(T);
-  return (cell3_cpb<K, GEOM, T>() * 3 * NV + E - 1) / E * E;
+  (void)NV;
+  return (cell3_cpb<K, GEOM, T>() * cell3_cs<K, GEOM, T>() + E - 1) / E * E;
 }
 template <int K, int GEOM, class T>
 __host__ __device__ constexpr int cell3_chunk() {
@@ -537,7 +556,8 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
                                                      T *__restrict__ dst, const T *__restrict__ metric,
                                                      int64_t cbeg, int64_t cend, const __grid_constant__ HexDev hx) {
   constexpr int N = K + 1, NP = N * N, NV = NP * N;
-  constexpr int CS = 3 * NV;  // U, G0, G1 per cell (the z-gradient lives in registers)
+  constexpr int CS = cell3_cs<K, GEOM, T>();  // U, G0, G1 per cell (the z-gradient lives in registers)
+  constexpr int AS = cell3_as<K, GEOM, T>();
   constexpr int cpb = cell3_cpb<K, GEOM, T>();
   extern __shared__ __align__(16) unsigned char smraw[];
   T *const sm = reinterpret_cast<T *>(smraw);
@@ -546,7 +566,7 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
   const bool active = cl < cpb;
   const int64_t cell0 = cbeg + (int64_t)blockIdx.x * cpb, cell = cell0 + cl;  // cells [cbeg, cend)
   const bool valid = active && cell < cend;
-  T *U = sm + (active ? cl : 0) * CS, *G0 = U + NV, *G1 = U + 2 * NV;
+  T *U = sm + (active ? cl : 0) * CS, *G0 = U + AS, *G1 = U + 2 * AS;
   T gz[N];  // z-pencil: Co_z Q (steps 3-5), then Co_z^T t_z (steps 5-7)
   // curved cells: the block's metric [6][cpb][NV] is staged into shared memory by
   // cp.async at kernel start, so its HBM latency overlaps steps 1-4
@@ -596,9 +616,16 @@ __global__ void __launch_bounds__(256) k_apply_cell3(const __grid_constant__ typ
   int o0[N], o1[N], o2[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    o0[i] = pen_off<3, N>(0, p, i);
-    o1[i] = pen_off<3, N>(1, p, i);
-    o2[i] = pen_off<3, N>(2, p, i);
+    if constexpr (cell3_padded<K, GEOM, T>()) {
+      const int u = p % N, w = p / N;
+      o0[i] = 54 * w + N * u + i;  // x-pencil (y = u, z = w)
+      o1[i] = 54 * w + N * i + u;  // y-pencil (x = u, z = w)
+      o2[i] = 54 * i + N * w + u;  // z-pencil (x = u, y = w)
+    } else {
+      o0[i] = pen_off<3, N>(0, p, i);
+      o1[i] = pen_off<3, N>(1, p, i);
+      o2[i] = pen_off<3, N>(2, p, i);
+    }
   }
   const int64_t Nx = g.N[0], plane = g.N[0] * g.N[1];
   const CellInfo ci = GEOM == 3 ? CellInfo{} : cell_info<3, K>(g, valid ? cell : ncells, ncells);
