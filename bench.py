@@ -97,13 +97,16 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # the first queries on a fresh box are slow; pay them before the timed region
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         except Exception:
             self.nv = None
 
     def _run(self):
         while not self._stop.is_set():
             self.sample()
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def sample(self):
         if self.nv is None:
