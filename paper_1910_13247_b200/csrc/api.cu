@@ -444,6 +444,7 @@ static int chosen_variant(const mf_op *op) {
   if (op->hex) return kVariantHex;
   if (op->dg) return kVariantDG;
   if (op->variant != kVariantAuto) return op->variant;
+  if (cart_halo_supported(op->g)) return kVariantCartHalo;
   return cart_plane_supported(op->g) ? kVariantCartPlane : kVariantGeneral;
 }
 
@@ -453,7 +454,12 @@ extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
   if ((variant == kVariantCartTile && !cart_tile_supported(op->g)) ||
       (variant == kVariantCartPlane && !cart_plane_supported(op->g)))
     return fail(MF_ERR_ARGUMENT, "tile/plane kernels need dim 3, Cartesian geometry, constant coefficient, k 2..4");
-  if (variant < 0 || variant > kVariantCartPlane) return fail(MF_ERR_ARGUMENT, "unknown variant");
+  if (variant == kVariantCartHalo && !cart_halo_supported(op->g))
+    return fail(MF_ERR_ARGUMENT,
+                "halo kernel needs dim 3, Cartesian, constant coefficient, k 4, n_cells x <= 256, and Dirichlet "
+                "x+ / y+ faces when n_cells x % 32 == 0 / n_cells y % 2 == 0");
+  if (variant < 0 || (variant > kVariantCartPlane && variant != kVariantCartHalo))
+    return fail(MF_ERR_ARGUMENT, "unknown variant");
   op->variant = variant;
   return MF_OK;
 }
@@ -508,7 +514,9 @@ static mf_status timing_mark(mf_op *op) {
 // (the interior layers, which never touch the shared planes) runs on stream
 static mf_status apply_split(mf_op *op, const double *src, double *dst, int var) {
   STATUS_TRY(timing_mark(op));
-  if (var == kVariantCartPlane) {
+  if (var == kVariantCartHalo) {
+    CUDA_TRY(launch_apply_cart_halo(op->g, op->t, src, dst, op->stream, &op->launches, 1));
+  } else if (var == kVariantCartPlane) {
     CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches, 1));
   } else {
     CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
@@ -520,7 +528,9 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
     STATUS_TRY(halo_post(op, dst, op->comm_stream));
     CUDA_TRY(cudaEventRecord(op->ev_halo, op->comm_stream));
   }
-  if (var == kVariantCartPlane)
+  if (var == kVariantCartHalo)
+    CUDA_TRY(launch_apply_cart_halo(op->g, op->t, src, dst, op->stream, &op->launches, 2));
+  else if (var == kVariantCartPlane)
     CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches, 2));
   else
     CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches, 2));
@@ -549,6 +559,10 @@ static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
   if (var == kVariantCartTile) {
     STATUS_TRY(timing_mark(op));
     CUDA_TRY(launch_apply_cart_tile(op->g, op->t, src, dst, op->stream, &op->launches));
+    STATUS_TRY(timing_mark(op));
+  } else if (var == kVariantCartHalo) {
+    STATUS_TRY(timing_mark(op));
+    CUDA_TRY(launch_apply_cart_halo(op->g, op->t, src, dst, op->stream, &op->launches));
     STATUS_TRY(timing_mark(op));
   } else if (var == kVariantCartPlane) {
     STATUS_TRY(timing_mark(op));
@@ -605,7 +619,9 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
   const int C = (pe && std::atoi(pe) > 0) ? std::atoi(pe) : 8;
   const int var = chosen_variant(op);
   const bool pipelined = !op->hex && op->world == 1 && g.dim == 3 &&
-                         (var == kVariantCartPlane || var == kVariantGeneral || var == kVariantDG) && C > 1 &&
+                         (var == kVariantCartPlane || var == kVariantCartHalo || var == kVariantGeneral ||
+                          var == kVariantDG) &&
+                         C > 1 &&
                          g.nc[2] >= 2 * C;
   if (!pipelined) {
     CUDA_TRY(cudaMemcpyAsync(op->h_src, src_host, bytes, cudaMemcpyHostToDevice, op->stream));
@@ -664,7 +680,10 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
                              cudaMemcpyHostToDevice, op->h2d_s));
     CUDA_TRY(cudaEventRecord(op->ev_in[r], op->h2d_s));
     CUDA_TRY(cudaStreamWaitEvent(op->stream, op->ev_in[r], 0));
-    if (var == kVariantCartPlane) {
+    if (var == kVariantCartHalo) {  // owner-writes: no zeroing, planes shared with range r+1 written there
+      CUDA_TRY(launch_apply_cart_halo(g, op->t, op->h_src, op->h_dst, op->stream, &op->launches, 3, (int)z0,
+                                      (int)z1));
+    } else if (var == kVariantCartPlane) {
       CUDA_TRY(launch_apply_cart_plane_range(g, op->t, op->h_src, op->h_dst, op->stream, &op->launches, (int)z0,
                                              (int)z1));
     } else {  // zero the planes no earlier range has touched, then add this range's cells
@@ -852,7 +871,7 @@ mf_status apply_f32(mf_op *op, const float *src, float *dst) {
   if (op->world != 1 || op->g.dim != 3 || op->dg || op->hex)
     return fail(MF_ERR_ARGUMENT, "FP32 apply: 3D CG brick, one rank");
   STATUS_TRY(ensure_f32(op));
-  if (chosen_variant(op) == kVariantCartPlane) {
+  if (chosen_variant(op) == kVariantCartPlane || chosen_variant(op) == kVariantCartHalo) {
     CUDA_TRY(launch_apply_cart_plane_f32(op->g, op->t, src, dst, op->stream, &op->launches));
   } else {
     CUDA_TRY(launch_zero_f(dst, op->n_local, op->stream, &op->launches));

@@ -62,6 +62,7 @@ enum Variant {
   kVariantCartPlane = 3, // Cartesian constant-coefficient 3D, 2D-first / z-last form
   kVariantDG = 4,        // mf_create_dg (reported by mf_get_info)
   kVariantHex = 5,       // mf_create_hex (reported by mf_get_info)
+  kVariantCartHalo = 6,  // Cartesian constant-coefficient 3D k = 4: owner-writes, no init / atomics
 };
 
 // Kernel launchers (return cudaError_t of the launch).
@@ -89,6 +90,11 @@ cudaError_t launch_apply_general_cells(const Geo &g, const Tables &t, const doub
 cudaError_t launch_apply_general_f32(const Geo &g, const Tables &t, const float *src, float *dst,
                                      const float *metric, cudaStream_t s, int64_t *launches);
 bool cart_plane_supported(const Geo &g);
+// kernels_halo.cu: part 0 = every layer, 1 = the two boundary layers, 2 = the interior
+// layers, 3 = the cell layers [zr_lo, zr_hi) (no dst initialisation needed in any part)
+cudaError_t launch_apply_cart_halo(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+                                   int64_t *launches, int part = 0, int zr_lo = 0, int zr_hi = 0);
+bool cart_halo_supported(const Geo &g);
 // DG-SIP operator and its diagonal (kernels_dg.cu, §8(f) f4)
 // cells [cbeg, cend) only (cend < 0: every cell); DoFs cell-major, plain stores
 cudaError_t launch_apply_dg(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
