@@ -59,7 +59,8 @@ constexpr int HMAXCH = 64;                 // z-chunks per launch
 constexpr int HMAXCLU = 8;                 // portable cluster size -> n_cells x <= 256
 constexpr int NB = 3;                      // a/b buffers (producer lead)
 constexpr int NS = 3;                      // producer input stages (cp.async ring: 2 steps of prefetch)
-constexpr int PROD_REGS = 88, CONS_REGS = 168;  // per-role register budgets (setmaxnreg; sum 256 = 2 x 128)
+constexpr int PROD_REGS = 104, CONS_REGS = 152;
+constexpr int PFD = 0;                     // L2 prefetch distance beyond the staged steps (0: off)  // per-role register budgets (setmaxnreg; sum 256 = 2 x 128)
 // Column-128 slots (written by the right CTA's producers) and x-halo slots (written by the
 // left CTA's consumers, one per layer).  The right CTA's producer reaches step t + DCOL only
 // after its consumers finished step t + DCOL - NB, whose node-0 completion waited for this
@@ -165,20 +166,39 @@ __device__ __forceinline__ void bar_expect(unsigned a, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void bar_wait(unsigned a, unsigned parity) {
+__device__ __forceinline__ bool bar_try(unsigned a, unsigned parity) {
+  unsigned ok;
   asm volatile(
-      "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W%=;\n}\n" ::"r"(a),
-      "r"(parity)
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// waiting warps back off (they would otherwise take issue slots from the working ones)
+__device__ __forceinline__ void bar_wait(unsigned a, unsigned parity) {
+#ifdef HALO_NOSYNC
+  return;
+#endif
+  while (!bar_try(a, parity)) __nanosleep(64);
 }
 // wait for data that other CTAs of the cluster delivered with st.async
 __device__ __forceinline__ void bar_wait_cluster(unsigned a, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W%=;\n}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
+#ifdef HALO_NOSYNC
+  return;
+#endif
+  while (true) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(64);
+  }
 }
 // two doubles into CTA `rank`'s shared memory at the offset of `local`, completing 16 bytes
 // on that CTA's mbarrier at the offset of `bar`
@@ -219,13 +239,19 @@ __global__ void __launch_bounds__(HNT, 1)
   const int nsteps = 1 + 2 * (cz_e - Ls);        // init plane + two steps per layer
   auto col_bytes = [](int t) { return t == 0 ? 8u * 2 * HROWS : 8u * 4 * HROWS; };
   auto hl_bytes = [&](int L) { return 8u * 2 * HROWS * (HK + (L == Ls ? 1 : 0)); };
+#ifdef HALO_PROF
   const int cta = blockIdx.x + gridDim.x * blockIdx.y;
+#endif
+  #ifdef HALO_PROF
   unsigned long long *const prof = P.prof ? P.prof + (size_t)cta * 640 : nullptr;
+#else
+  constexpr unsigned long long *prof = nullptr;
+#endif
   if (prof && tid == 0) prof[0] = gtimer();
 
   // ---- init: zero the exchange slots (stay 0 where there is no neighbour), barriers, and the
   // expected bytes of the first uses of the exchange slots
-  for (int i = tid; i < DCOL * COL_SLOT + DHL * HL_SLOT; i += HNT) COL[i] = 0.0;
+  for (int i = tid; i < DCOL * COL_SLOT + DHL * HL_SLOT + NS * US_STAGE; i += HNT) COL[i] = 0.0;
   if (tid == 0) {
     for (int b = 0; b < NB; ++b) {
       bar_init(b_full + 8 * b, HROWS);  // one elected arrival per warp
@@ -233,6 +259,7 @@ __global__ void __launch_bounds__(HNT, 1)
     }
     for (int s = 0; s < DCOL; ++s) bar_init(b_col + 8 * s, 1);
     for (int s = 0; s < DHL; ++s) bar_init(b_hl + 8 * s, 1);
+
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     if (!last_x)
       for (int s = 0; s < DCOL && s < nsteps; ++s) bar_expect(b_col + 8 * s, col_bytes(s));
@@ -259,16 +286,20 @@ __global__ void __launch_bounds__(HNT, 1)
       if (colin && y >= 0 && y < Ny) inmask |= 1u << i;
       if (((d & 4u) && y == 0) || ((d & 8u) && y == Ny - 1)) consmask |= 1u << i;
     }
-    const bool halo_y = ty > 0, cell1_y = nvy > 1, allin = inmask == (1u << HYR) - 1;
+    const bool halo_y = ty > 0, cell1_y = nvy > 1;
     // the x+ column of a full last CTA (column 128, Dirichlet by the host check): identity
     // rows written by the two producers of column 127
     const bool col128 = ncol > HCOLS && yc == HCOLS - 1;
+    const bool wslow = __any_sync(0xffffffffu, !colin || colc || consmask != 0 || col128);
     auto plane_of = [&](int t) {
       return t == 0 ? (int64_t)HK * Ls : (int64_t)HK * (Ls + (t - 1) / 2) + 1 + ((t - 1) & 1) + 2 * yj;
     };
-    // step t's inputs -> stage t % NS (cp.async; rows outside the mesh are zero-filled)
+    // step t's inputs -> stage t % NS (cp.async, one node per thread and row; rows outside the
+    // mesh are never loaded: their stage slots stay 0 from the start)
+    const bool allin = inmask == (1u << HYR) - 1;
     auto load = [&](int t) {
       if (t < nsteps && (t > 0 || yj == 0)) {
+#ifndef HALO_NOLOAD
         const int64_t gz = plane_of(t);
         const double *s0 = src + gz * plane + (y0 - HK) * Nx + gx;
         double *st = US + (t % NS) * US_STAGE + yt;
@@ -277,131 +308,141 @@ __global__ void __launch_bounds__(HNT, 1)
           for (int i = 0; i < HYR; ++i) cp_async_z<double>(st + i * 32 * HROWS, s0 + i * Nx, 8u);
         } else {
 #pragma unroll
-          for (int i = 0; i < HYR; ++i) {
-            const bool in = (inmask >> i) & 1u;
-            cp_async_z<double>(st + i * 32 * HROWS, in ? s0 + i * Nx : src, in ? 8u : 0u);
-          }
+          for (int i = 0; i < HYR; ++i)
+            if ((inmask >> i) & 1u) cp_async_z<double>(st + i * 32 * HROWS, s0 + i * Nx, 8u);
         }
         if (col128) {
           const double *s1 = src + gz * plane + y0 * Nx + gx + 1;
           double *c = C128 + (gz % C128_RING) * (HROWS + 1);
 #pragma unroll
-          for (int r = 0; r <= HROWS; ++r) cp_async_z<double>(c + r, r < nrow ? s1 + r * Nx : src, r < nrow ? 8u : 0u);
+          for (int r = 0; r <= HROWS; ++r)
+            if (r < nrow) cp_async_z<double>(c + r, s1 + r * Nx, 8u);
         }
+#endif
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
+#ifdef HALO_ONLY_CONS  // (timing experiment: the producers only hand over buffers)
+    for (int t = 0; t < nsteps; ++t) {
+      if (t >= NB) bar_wait(b_empty + 8 * (t % NB), ((t / NB) - 1) & 1);
+      __syncwarp();
+      if (lane == 0) bar_arrive(b_full + 8 * (t % NB));
+    }
+    if (nsteps < 0)
+#endif
+    {
     for (int t = 0; t < NS - 1; ++t) load(t);
     for (int t = 0; t < nsteps; ++t) {
-      if (prof && lane == 0 && t >= 10 && t < 20) prof[160 + (w - HROWS) * 30 + (t - 10) * 3] = gtimer();
       load(t + NS - 1);
       asm volatile("cp.async.wait_group %0;\n" ::"n"(NS - 1) : "memory");
-      double u[HYR];
-      {
-        const double *st = US + (t % NS) * US_STAGE + yt;
-#pragma unroll
-        for (int i = 0; i < HYR; ++i) u[i] = st[i * 32 * HROWS];
-      }
       const int64_t gz = plane_of(t);
       const bool on = t > 0 || yj == 0;
-      const bool zc = ((d & 16u) && gz == 0) || ((d & 32u) && gz == Nz - 1);
-      const bool outp = gz >= (int64_t)HK * cz_b && (gz < (int64_t)HK * cz_e || (cz_e == P.ncz && gz == Nz - 1));
-      if ((zc || colc || consmask) && on && outp) {  // identity rows of this plane
-        const bool skipid = P.skip_top_identity && gz == Nz - 1;
-        double *d0 = dst + gz * plane + y0 * Nx + gx;
-        {
+      double u[HYR];
+      {
+        // rows outside the mesh are never copied (their stage rows stay 0 from the start)
+        const int p0 = (int)((gz + (y0 - HK) + x0) & 1);  // Nx, plane odd: row i starts at parity p0 ^ (i & 1)
+        const double *st = US + (t % NS) * US_STAGE + yt;
+        (void)p0;
 #pragma unroll
-          for (int r = 0; r <= HROWS; ++r)
-            if (r < nrow && yc < ncol && (zc || colc || ((consmask >> (r + HK)) & 1u))) d0[r * Nx] = skipid ? 0.0 : u[r + HK];
+        for (int i = 0; i < HYR; ++i) u[i] = st[i * 32 * HROWS];
+        const bool zc = ((d & 16u) && gz == 0) || ((d & 32u) && gz == Nz - 1);  // a Dirichlet z plane
+        if (wslow || zc) {  // warp with columns outside the mesh, Dirichlet nodes or the x+ column
+          const bool outp = gz >= (int64_t)HK * cz_b && (gz < (int64_t)HK * cz_e || (cz_e == P.ncz && gz == Nz - 1));
+          if ((zc || colc || consmask) && on && outp && colin) {  // identity rows (R3) with the loaded values
+            const bool skipid = P.skip_top_identity && gz == Nz - 1;
+            double *d0 = dst + gz * plane + y0 * Nx + gx;
+#pragma unroll
+            for (int r = 0; r <= HROWS; ++r)
+              if (r < nrow && yc < ncol && (zc || colc || ((consmask >> (r + HK)) & 1u)))
+                d0[r * Nx] = skipid ? 0.0 : u[r + HK];
+          }
+          if (zc || colc || !colin) {
+#pragma unroll
+            for (int i = 0; i < HYR; ++i) u[i] = 0.0;
+          } else if (consmask) {
+#pragma unroll
+            for (int i = 0; i < HYR; ++i)
+              if ((consmask >> i) & 1u) u[i] = 0.0;
+          }
         }
       }
-      if (zc || colc) {
-#pragma unroll
-        for (int i = 0; i < HYR; ++i) u[i] = 0.0;
-      } else if (consmask) {
-#pragma unroll
-        for (int i = 0; i < HYR; ++i)
-          if ((consmask >> i) & 1u) u[i] = 0.0;
-      }
-      const int b = t % NB;
-      if (t >= NB) bar_wait(b_empty + 8 * b, ((t / NB) - 1) & 1);
-      if (prof && yt == 0 && t < 24) prof[100 + 2 * t] = gtimer();
-      if (prof && lane == 0 && t >= 10 && t < 20) prof[160 + (w - HROWS) * 30 + (t - 10) * 3 + 1] = gtimer();
-      if (on) {
-        // y step, stored as it goes: the top row of the cell below (rows 0..4 of u), cell 0
-        // (u rows 4..8 -> tile rows 0..4), cell 1 (u rows 8..12 -> tile rows 4..8)
-        double *pa = AB + b * AB_BUF + yj * AB_PL + hxs(yc);
-        double *pb = pa + 2 * AB_PL;
-        double e[3], o[2], ve[3], vo[2], a0[5], b0[5];
+      // y step into registers first (three independent chains: the top row of the cell below
+      // from u rows 0..4, cell 0 from rows 4..8, cell 1 from rows 8..12), then the buffer
+      double av[HROWS], bv[HROWS];
+      {
+        double e[3], o[2], f[3], g[3], ve[3], vo[2], a0[5], b0[5], a1[5], b1[5];
         double ha = 0.0, hb = 0.0;
         if (halo_y) {  // row 4 of the cell below = ve_0 - vo_0 of its even-odd product
-          split5(u, e, o);
-          ha = fma(P.M.E[0][2], e[2], fma(P.M.E[0][1], e[1], P.M.E[0][0] * e[0])) -
-               fma(P.M.O[0][1], o[1], P.M.O[0][0] * o[0]);
-          hb = fma(P.K.E[0][2], e[2], fma(P.K.E[0][1], e[1], P.K.E[0][0] * e[0])) -
-               fma(P.K.O[0][1], o[1], P.K.O[0][0] * o[0]);
+          double he[3], ho[2];
+          split5(u, he, ho);
+          ha = fma(P.M.E[0][2], he[2], fma(P.M.E[0][1], he[1], P.M.E[0][0] * he[0])) -
+               fma(P.M.O[0][1], ho[1], P.M.O[0][0] * ho[0]);
+          hb = fma(P.K.E[0][2], he[2], fma(P.K.E[0][1], he[1], P.K.E[0][0] * he[0])) -
+               fma(P.K.O[0][1], ho[1], P.K.O[0][0] * ho[0]);
           if (!ISO) hb *= ry;
         }
         split5(u + 4, e, o);
+        split5(u + 8, f, g);
         mul5(P.M, e, o, ve, vo);
         comb5(ve, vo, a0);
+        mul5(P.M, f, g, ve, vo);
+        comb5(ve, vo, a1);
         mul5(P.K, e, o, ve, vo);
         comb5(ve, vo, b0);
+        mul5(P.K, f, g, ve, vo);
+        comb5(ve, vo, b1);
         if (!ISO) {
 #pragma unroll
-          for (int i = 0; i < 5; ++i) b0[i] *= ry;
-        }
-        a0[0] += ha;
-        b0[0] += hb;
-        const bool sendc = yc == 0 && rank > 0;  // column 0 -> the left CTA's column-128 slot
-        const int sc = t % DCOL;
-        double *cs = COL + sc * COL_SLOT + yj * 2 * HROWS;
-#pragma unroll
-        for (int r = 0; r < HK; ++r) {
-          pa[r * HXP] = a0[r];
-          pb[r * HXP] = b0[r];
-        }
-        if (sendc) {
-          st_async2(cs + 0, b_col + 8 * sc, rank - 1, a0[0], a0[1]);
-          st_async2(cs + 2, b_col + 8 * sc, rank - 1, a0[2], a0[3]);
-          st_async2(cs + HROWS + 0, b_col + 8 * sc, rank - 1, b0[0], b0[1]);
-          st_async2(cs + HROWS + 2, b_col + 8 * sc, rank - 1, b0[2], b0[3]);
-        }
-        double a4 = a0[HK], b4 = b0[HK];
-        if (cell1_y) {
-          split5(u + 8, e, o);
-          mul5(P.M, e, o, ve, vo);
-          comb5(ve, vo, a0);
-          mul5(P.K, e, o, ve, vo);
-          comb5(ve, vo, b0);
-          if (!ISO) {
-#pragma unroll
-            for (int i = 0; i < 5; ++i) b0[i] *= ry;
+          for (int i = 0; i < 5; ++i) {
+            b0[i] *= ry;
+            b1[i] *= ry;
           }
-          a0[0] += a4;
-          b0[0] += b4;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 5; ++i) a0[i] = b0[i] = 0.0;
-          a0[0] = a4;
-          b0[0] = b4;
         }
+        if (!cell1_y) {
 #pragma unroll
-        for (int r = 0; r < HK; ++r) {
-          pa[(HK + r) * HXP] = a0[r];
-          pb[(HK + r) * HXP] = b0[r];
+          for (int i = 0; i < 5; ++i) a1[i] = b1[i] = 0.0;
         }
-        if (sendc) {
-          st_async2(cs + 4, b_col + 8 * sc, rank - 1, a0[0], a0[1]);
-          st_async2(cs + 6, b_col + 8 * sc, rank - 1, a0[2], a0[3]);
-          st_async2(cs + HROWS + 4, b_col + 8 * sc, rank - 1, b0[0], b0[1]);
-          st_async2(cs + HROWS + 6, b_col + 8 * sc, rank - 1, b0[2], b0[3]);
+        av[0] = a0[0] + ha;
+        bv[0] = b0[0] + hb;
+#pragma unroll
+        for (int r = 1; r < HK; ++r) {
+          av[r] = a0[r];
+          bv[r] = b0[r];
+          av[HK + r] = a1[r];
+          bv[HK + r] = b1[r];
+        }
+        av[HK] = a0[HK] + a1[0];
+        bv[HK] = b0[HK] + b1[0];
+      }
+      const int b = t % NB;
+#ifndef HALO_NOEMPTY
+      if (t >= NB) bar_wait(b_empty + 8 * b, ((t / NB) - 1) & 1);
+#endif
+      if (prof && yt == 0 && t < 24) prof[100 + 2 * t] = gtimer();
+      if (prof && lane == 0 && t >= 10 && t < 20) prof[160 + (w - HROWS) * 30 + (t - 10) * 3 + 1] = gtimer();
+      if (on) {
+        double *pa = AB + b * AB_BUF + yj * AB_PL + hxs(yc);
+        double *pb = pa + 2 * AB_PL;
+#pragma unroll
+        for (int r = 0; r < HROWS; ++r) {
+          pa[r * HXP] = av[r];
+          pb[r * HXP] = bv[r];
+        }
+        if (yc == 0 && rank > 0) {  // column 0 -> the left CTA's column-128 slot of this step
+          const int sc = t % DCOL;
+          double *cs = COL + sc * COL_SLOT + yj * 2 * HROWS;
+#pragma unroll
+          for (int r = 0; r < HROWS; r += 2) {
+            st_async2(cs + r, b_col + 8 * sc, rank - 1, av[r], av[r + 1]);
+            st_async2(cs + HROWS + r, b_col + 8 * sc, rank - 1, bv[r], bv[r + 1]);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) bar_arrive(b_full + 8 * b);
       if (prof && yt == 0 && t < 24) prof[101 + 2 * t] = gtimer();
       if (prof && lane == 0 && t >= 10 && t < 20) prof[160 + (w - HROWS) * 30 + (t - 10) * 3 + 2] = gtimer();
+    }
     }
   } else {
     // ================= consumer warps: x and z steps, stores =================
@@ -508,7 +549,9 @@ __global__ void __launch_bounds__(HNT, 1)
       }
       if (rank > 0) {
         const int s = (L - Ls) % DHL;
+#ifndef HALO_ONLY_CONS
         bar_wait_cluster(b_hl + 8 * s, ((L - Ls) / DHL) & 1);
+#endif
         if (lane == 0) {
           const double *h = HL + s * HL_SLOT + w * 2;
           if (L == Ls) {
@@ -547,6 +590,14 @@ __global__ void __launch_bounds__(HNT, 1)
       }
     };
 
+#ifdef HALO_ONLY_PROD  // (timing experiment: the consumers only hand over buffers)
+    for (int t = 0; t < nsteps; ++t) {
+      bar_wait(b_full + 8 * (t % NB), (t / NB) & 1);
+      __syncwarp();
+      if (lane == 0) bar_arrive(b_empty + 8 * (t % NB));
+    }
+    if (nsteps < 0)
+#endif
     for (int t = 0; t <= nsteps; ++t) {
       if (t == nsteps) {  // drain: node 0 of the last layer, then the top plane of the mesh
         finish_node0(cz_e - 1);
@@ -560,10 +611,14 @@ __global__ void __launch_bounds__(HNT, 1)
       const int b = t % NB, s = t % DCOL;
       const int L = Ls + (t - 1) / 2, h = (t - 1) & 1;
       if (prof && tid == 0 && t < 28) prof[2 + t] = gtimer();
+#ifndef HALO_NOFULL
       bar_wait(b_full + 8 * b, (t / NB) & 1);
+#endif
       if (prof && tid == 0 && t < 24) prof[30 + 3 * t] = gtimer();
       if (prof && lane == 0 && t >= 10 && t < 20) prof[400 + w * 30 + (t - 10) * 3] = gtimer();
+#ifndef HALO_ONLY_CONS
       if (!last_x) bar_wait_cluster(b_col + 8 * s, (t / DCOL) & 1);
+#endif
       if (prof && tid == 0 && t < 24) prof[31 + 3 * t] = gtimer();
       if (t == 0) {
         double Pv[5], Qv[5];
@@ -734,6 +789,10 @@ bool cart_halo_supported(const Geo &g) {
 // interior layers; 3: the layers [zr_lo, zr_hi) only
 cudaError_t launch_apply_cart_halo(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
                                    int64_t *launches, int part, int zr_lo, int zr_hi) {
+  if ((reinterpret_cast<uintptr_t>(src) & 15) != 0) {  // TMA bulk copies need 16-byte aligned rows
+    if (part == 3) return launch_apply_cart_plane_range(g, t, src, dst, s, launches, zr_lo, zr_hi);
+    return launch_apply_cart_plane(g, t, src, dst, s, launches, part);
+  }
   HaloParams P;
   std::memset(&P, 0, sizeof(P));
   eo5_from(t.Mr, 1.0, &P.M);
@@ -788,7 +847,11 @@ cudaError_t launch_apply_cart_halo(const Geo &g, const Tables &t, const double *
   cfg.attrs = attr;
   cfg.numAttrs = P.ntx > 1 ? 1 : 0;
   ++*launches;
+#ifdef HALO_PROF
   static const bool profile = std::getenv("MF_HALO_PROF") != nullptr;
+#else
+  constexpr bool profile = false;
+#endif
   if (!profile) return cudaLaunchKernelEx(&cfg, kern, P, src, dst);
   // debug timeline: per-CTA start / per-step (consumer warp 0) / end, printed to stderr
   const int ncta = P.ntx * P.nty * P.nch;

@@ -92,7 +92,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = path or _build.LIB
+    path = path or os.environ.get("MF_LIB_PATH") or _build.LIB  # (MF_LIB_PATH: kernel experiments)
     if not os.path.exists(path):
         raise RuntimeError(f"{path} missing: run `python -m paper_1910_13247_b200.build` (no CPU fallback)")
     L = ctypes.CDLL(path)

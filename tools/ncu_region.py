@@ -58,7 +58,7 @@ for name, c in reg.items():
     reasons = sorted(((v, k) for k, v in c.items() if k.startswith("stall_")), reverse=True)[:6]
     print(f"{name:16s} samples {c[S] / tot * 100:5.1f}%  inst {c['Instructions Executed']}  " +
           " ".join(f"{k[6:]}={v / tot * 100:.1f}" for v, k in reasons))
-for name in ("consumer", "producer"):
+for name in ("other", "consumer", "producer"):
     print("== top lines:", name)
     lines = sorted(((c[S], k) for k, c in agg.items() if region(k) == name), reverse=True)[:top]
     for v, (f, ln) in lines:
