@@ -814,7 +814,32 @@ cudaError_t launch_apply_cart_halo(const Geo &g, const Tables &t, const double *
   int sms = 0;
   cudaError_t e = halo_prepare(&sms);
   if (e != cudaSuccess) return e;
-  const int slots = std::max(1, sms / P.ntx);  // clusters resident at one CTA per SM
+  // clusters resident at once (one CTA per SM; a cluster's CTAs share a GPC, so wide clusters
+  // fit fewer times than sms / ntx)
+  int slots = std::max(1, sms / P.ntx);
+  {
+    static int cached[HMAXCLU + 1] = {};
+    if (cached[P.ntx] == 0) {
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3((unsigned)P.ntx, 1);
+      qc.blockDim = dim3(HNT);
+      qc.dynamicSmemBytes = HSMEM;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = (unsigned)P.ntx;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k_apply_halo<true>, &qc) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = slots;
+      }
+      cached[P.ntx] = n;
+    }
+    slots = std::min(slots, cached[P.ntx]);
+  }
   std::vector<std::pair<int, int>> ch;
   const int ncz = P.ncz;
   if (part == 0) {
