@@ -28,7 +28,11 @@
  *    n_local): its DoF planes plus a duplicate of the shared upper plane
  *    (owned, for dot products, by the upper rank; the first n_owned entries are
  *    this rank's owned DoFs).  Every call is then collective (same order and
- *    arguments on every rank, as in NCCL).
+ *    arguments on every rank, as in NCCL).  The blocking calls (mf_cg_solve,
+ *    mf_estimate_lambda_max, mf_apply_host, mf_sync) poll ncclCommGetAsyncError
+ *    while they wait; an NCCL error, or no progress for MF_NCCL_TIMEOUT_S seconds
+ *    (environment, default 300), aborts the communicator (ncclCommAbort) and
+ *    returns MF_ERR_NCCL -- the op is unusable afterwards (destroy it).
  *  - Errors: negative mf_status, message from mf_last_error() (thread-local).
  *    An op is not thread-safe.
  */
@@ -182,6 +186,20 @@ mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_src, double
  * §8(f) f2).  3D, world_size 1 only (else MF_ERR_ARGUMENT).
  * Asynchronous. */
 mf_status mf_apply_f32(mf_op *op, const float *src, int64_t n_src, float *dst, int64_t n_dst);
+
+/* Testing hook for the overlapped multi-GPU apply (§8(e)): runs
+ * ONE part of its launch sequence on one GPU, without the exchange -- part 1 = the
+ * cell layers next to the shared z-planes (and, for kernels that need it, the
+ * initialisation of dst), part 2 = the interior layers, which never write the
+ * shared planes (first and last plane of the local vector) and never read dst.
+ * Part 1 followed by part 2 is mf_apply on one rank.  3D brick operators only
+ * (MF_ERR_ARGUMENT otherwise, or part not 1 / 2).  Asynchronous. */
+mf_status mf_apply_split_part(mf_op *op, const double *src, int64_t n_src, double *dst, int64_t n_dst,
+                              int32_t part);
+
+/* Waits for the op's stream (and, with world_size > 1, watches the communicator as
+ * described above).  MF_ERR_NCCL after an abort. */
+mf_status mf_sync(mf_op *op);
 
 /* diag = diagonal of A (§8(a) a9), 1 on constrained DoFs.  Asynchronous. */
 mf_status mf_diagonal(mf_op *op, double *diag, int64_t n);

@@ -4,7 +4,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <thread>
 #include <functional>
 #include <cmath>
 #include <cstdio>
@@ -54,6 +56,7 @@ struct mf_op {
 };
 
 static thread_local std::string g_err;
+static mf_status stream_wait(mf_op *op);
 
 static mf_status fail(mf_status s, const std::string &msg) {
   g_err = msg;
@@ -467,6 +470,7 @@ extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
 // symmetric exchange of the partial sums on shared z-planes (§8(e)):
 // send my partial of each shared plane, receive the neighbour's (on stream s) ...
 static mf_status halo_post(mf_op *op, double *dst, cudaStream_t s) {
+  if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
   const int64_t np = op->plane;
   double *lo = dst, *hi = dst + op->n_local - np;
   const bool has_lo = op->rank > 0, has_hi = op->rank < op->world - 1;
@@ -538,6 +542,25 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
   if (op->world > 1) {
     CUDA_TRY(cudaStreamWaitEvent(op->stream, op->ev_halo, 0));
     STATUS_TRY(halo_add(op, dst));
+  }
+  return MF_OK;
+}
+
+extern "C" mf_status mf_apply_split_part(mf_op *op, const double *src, int64_t n_src, double *dst, int64_t n_dst,
+                                         int32_t part) {
+  if (!op || !src || !dst) return fail(MF_ERR_ARGUMENT, "null argument");
+  if (n_src != op->n_local || n_dst != op->n_local) return fail(MF_ERR_LENGTH, "vector length != n_local");
+  if (op->hex || op->dg || op->g.dim != 3 || (part != 1 && part != 2))
+    return fail(MF_ERR_ARGUMENT, "split parts: 3D brick operator, part 1 or 2");
+  const int var = chosen_variant(op);
+  if (var == kVariantCartTile) return fail(MF_ERR_ARGUMENT, "the tile variant has no split");
+  if (var == kVariantCartHalo) {
+    CUDA_TRY(launch_apply_cart_halo(op->g, op->t, src, dst, op->stream, &op->launches, part));
+  } else if (var == kVariantCartPlane) {
+    CUDA_TRY(launch_apply_cart_plane(op->g, op->t, src, dst, op->stream, &op->launches, part));
+  } else {
+    if (part == 1) CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
+    CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches, part));
   }
   return MF_OK;
 }
@@ -627,7 +650,7 @@ extern "C" mf_status mf_apply_host(mf_op *op, const double *src_host, int64_t n_
     CUDA_TRY(cudaMemcpyAsync(op->h_src, src_host, bytes, cudaMemcpyHostToDevice, op->stream));
     STATUS_TRY(apply_impl(op, op->h_src, op->h_dst));
     CUDA_TRY(cudaMemcpyAsync(dst_host, op->h_dst, bytes, cudaMemcpyDeviceToHost, op->stream));
-    CUDA_TRY(cudaStreamSynchronize(op->stream));
+    STATUS_TRY(stream_wait(op));
     return MF_OK;
   }
   // Pipelined: the cell layers in C z-ranges; range r's input planes go up on h2d_s, its
@@ -734,14 +757,52 @@ static mf_status ensure_solver(mf_op *op) {
   return MF_OK;
 }
 
+// Wait for the op's stream.  With world_size > 1 the wait polls the communicator:
+// ncclCommGetAsyncError != ncclSuccess, or no completion within MF_NCCL_TIMEOUT_S seconds
+// (a peer died or hung), aborts it and returns MF_ERR_NCCL (SURVEY §5 failure detection).
+static mf_status stream_wait(mf_op *op) {
+  if (op->world == 1) {
+    CUDA_TRY(cudaStreamSynchronize(op->stream));
+    return MF_OK;
+  }
+  if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
+  static const double timeout_s = [] {
+    const char *e = std::getenv("MF_NCCL_TIMEOUT_S");
+    return e && std::atof(e) > 0 ? std::atof(e) : 300.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long it = 0;; ++it) {
+    cudaError_t q = cudaStreamQuery(op->stream);
+    if (q == cudaSuccess) return MF_OK;
+    if (q != cudaErrorNotReady) return fail(MF_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError(op->comm, &ar);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ar != ncclSuccess && ar != ncclInProgress) || el > timeout_s) {
+      ncclCommAbort(op->comm);
+      op->comm = nullptr;
+      return fail(MF_ERR_NCCL, ar != ncclSuccess ? std::string("NCCL async error: ") + ncclGetErrorString(ar)
+                                                  : std::string("no progress within MF_NCCL_TIMEOUT_S; "
+                                                                "communicator aborted"));
+    }
+    if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+extern "C" mf_status mf_sync(mf_op *op) {
+  if (!op) return fail(MF_ERR_ARGUMENT, "null op");
+  return stream_wait(op);
+}
+
 // nd dot products over the owned prefix, summed over ranks; result to host_scal[0..nd)
 static mf_status dots(mf_op *op, int nd, const double *const *a, const double *const *b) {
   CUDA_TRY(launch_dots(nd, a, b, op->n_owned, op->partials, op->dev_scal, op->stream, &op->launches));
-  if (op->world > 1)
+  if (op->world > 1) {
+    if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
     NCCL_TRY(ncclAllReduce(op->dev_scal, op->dev_scal, nd, ncclDouble, ncclSum, op->comm, op->stream));
+  }
   CUDA_TRY(cudaMemcpyAsync(op->host_scal, op->dev_scal, nd * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
-  CUDA_TRY(cudaStreamSynchronize(op->stream));
-  return MF_OK;
+  return stream_wait(op);
 }
 
 // largest eigenvalue of the symmetric tridiagonal (d, e) by Sturm-sequence bisection

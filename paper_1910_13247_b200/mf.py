@@ -82,7 +82,8 @@ EXPORTS = ["mf_create", "mf_destroy", "mf_last_error", "mf_nccl_unique_id", "mf_
            "mf_partition", "mf_mg_create", "mf_mg_destroy", "mf_mg_levels", "mf_mg_level_size", "mf_mg_level_op",
            "mf_mg_level_lambda", "mf_mg_prolongate", "mf_mg_restrict", "mf_mg_vcycle", "mf_mg_cg_solve",
            "mf_mg_set_stream", "mf_apply_f32", "mf_create_dg", "mf_hng_create", "mf_hng_destroy", "mf_hng_sizes",
-           "mf_hng_apply", "mf_hng_set_stream", "mf_create_hex", "mf_hex_number_dofs"]
+           "mf_hng_apply", "mf_hng_set_stream", "mf_create_hex", "mf_hex_number_dofs", "mf_apply_split_part",
+           "mf_sync"]
 
 _lib = None
 
@@ -131,6 +132,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
                            ctypes.c_int32],
         "mf_mg_set_stream": [vp, vp],
         "mf_apply_f32": [vp, vp, i64, vp, i64],
+        "mf_apply_split_part": [vp, vp, i64, vp, i64, ctypes.c_int32],
+        "mf_sync": [vp],
         "mf_create_dg": [ctypes.POINTER(Mesh), ctypes.c_int32, ctypes.POINTER(Coeff), ctypes.POINTER(vp)],
         "mf_hng_create": [dp, dp, ctypes.c_double, i64p, i64, ctypes.c_int32, ctypes.POINTER(Coeff),
                           ctypes.POINTER(vp)],
@@ -270,6 +273,8 @@ class Operator:
         t = self._torch
         if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float64 and x.is_contiguous()):
             raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+        if x.device != self.device:
+            raise TypeError(f"{name} is on {x.device}, the operator on {self.device}")
         return ctypes.c_void_p(x.data_ptr())
 
     def new_vector(self):
@@ -281,6 +286,18 @@ class Operator:
         self._stream()
         _check(load().mf_apply(self._h, self._vec(src, "src"), src.numel(), self._vec(dst, "dst"), dst.numel()))
         return dst
+
+    def apply_split_part(self, src, dst, part: int):
+        """One part of the overlapped multi-GPU launch sequence on this GPU (mf_apply_split_part:
+        1 = the cell layers next to the shared z-planes, 2 = the interior layers)."""
+        self._stream()
+        _check(load().mf_apply_split_part(self._h, self._vec(src, "src"), src.numel(), self._vec(dst, "dst"),
+                                          dst.numel(), int(part)))
+        return dst
+
+    def sync(self):
+        """mf_sync: wait for the op's stream (watching the communicator on N > 1)."""
+        _check(load().mf_sync(self._h))
 
     def apply_f32(self, src, dst=None):
         """The FP32 instance of the apply (mixed-precision multigrid); float32 CUDA tensors."""
@@ -296,7 +313,12 @@ class Operator:
 
     def apply_host(self, src: np.ndarray, dst: np.ndarray | None = None) -> np.ndarray:
         src = np.ascontiguousarray(src, dtype=np.float64)
-        dst = np.empty_like(src) if dst is None else dst
+        if dst is None:
+            dst = np.empty_like(src)
+        elif not (isinstance(dst, np.ndarray) and dst.dtype == np.float64 and dst.flags["C_CONTIGUOUS"]
+                  and dst.flags["WRITEABLE"] and dst.size == self.n_local):
+            # the C side writes n_local doubles through dst's data pointer
+            raise TypeError(f"dst must be a writeable C-contiguous float64 array of {self.n_local} entries")
         dp = ctypes.POINTER(ctypes.c_double)
         self._stream()
         _check(load().mf_apply_host(self._h, src.ctypes.data_as(dp), src.size, dst.ctypes.data_as(dp), dst.size))

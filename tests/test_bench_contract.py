@@ -52,3 +52,16 @@ def test_reference_arm_world2_rank0_only():
 def test_bench_rejects_unknown_arguments(bad):
     r = subprocess.run([sys.executable, "bench.py", *bad], cwd=ROOT, capture_output=True, text=True, timeout=120)
     assert r.returncode != 0
+
+
+def test_reference_arm_world2_default_is_strong_scaling_cfg5():
+    # N > 1 without --config: BASELINE configs[4], the 256^3 Q4 cube split over the ranks
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29534", "bench.py", "--impl", "reference",
+                        "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr
+    (d,) = _lines(r.stdout)
+    assert d["scaling"] == "strong" and d["config"]["config"] == "cfg5q4"
+    assert d["config"]["n_cells"] == [256, 256, 256] and d["config"]["n_dofs"] == 1025 ** 3

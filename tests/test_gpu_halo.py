@@ -116,3 +116,53 @@ def test_halo_cfg3_full_size_vs_kronecker_oracle(torch):
     assert rel_l2(y, y_ref) <= CUDA_ORACLE_TOL
     m = oracle.constrained_mask_fast(p)
     np.testing.assert_array_equal(y[m], x[m])
+
+
+SPLIT_CASES = [
+    (dict(dim=3, n_cells=(9, 17, 7), k=4), "halo"),
+    (dict(dim=3, n_cells=(40, 7, 11), k=4, dirichlet=0), "halo"),
+    (dict(dim=3, n_cells=(70, 3, 9), k=4, dirichlet=0b100110), "halo"),
+    (dict(dim=3, n_cells=(9, 10, 11), k=2), "plane"),
+    (dict(dim=3, n_cells=(6, 5, 7), k=3, geometry="sine", coeff="variable"), "general"),
+    (dict(dim=3, n_cells=(3, 3, 5), k=5), "general"),
+]
+
+
+@pytest.mark.parametrize("case,variant", SPLIT_CASES, ids=lambda v: v if isinstance(v, str) else _id(v))
+def test_split_interior_part_never_touches_the_shared_planes(case, variant, torch):
+    # §8(e) overlap: part 2 (interior layers) runs while NCCL reads the partial sums of the
+    # shared z-planes (the first and last plane of the local vector), so it must neither write
+    # them nor need them; part 1 + part 2 = mf_apply.  A finite sentinel pattern catches plain
+    # stores and atomic adds alike.
+    op = cuda_operator(case)
+    op.set_variant(variant)
+    n = op.n_local
+    plane = (case["k"] * case["n_cells"][0] + 1) * (case["k"] * case["n_cells"][1] + 1)
+    x = torch.from_numpy(seeded(n, 3)).cuda()
+    sentinel = torch.arange(n, dtype=torch.float64, device="cuda") * 1e-3 + 12345.0
+    dst = sentinel.clone()
+    op.apply_split_part(x, dst, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:plane], sentinel[:plane])
+    assert torch.equal(dst[-plane:], sentinel[-plane:])
+    # part 2 did write the interior (it is not a no-op) when there are interior layers
+    if case["n_cells"][2] > 2:
+        assert not torch.equal(dst[plane:-plane], sentinel[plane:-plane])
+    ref = op.apply(x)
+    both = sentinel.clone()
+    op.apply_split_part(x, both, 1)
+    op.apply_split_part(x, both, 2)
+    err = ((both - ref).norm() / ref.norm()).item()
+    assert err <= (0.0 if variant == "halo" else 1e-14), err
+
+
+def test_binding_argument_checks(torch):
+    op = cuda_operator(dict(dim=3, n_cells=(2, 2, 2), k=2))
+    x = seeded(op.n_local, 1)
+    with pytest.raises(TypeError):
+        op.apply_host(x, np.empty(op.n_local, dtype=np.float32))
+    with pytest.raises(TypeError):
+        op.apply_host(x, np.empty(2 * op.n_local)[::2])
+    with pytest.raises(TypeError):
+        op.apply(torch.from_numpy(x))  # a CPU tensor
+    op.sync()
