@@ -34,7 +34,9 @@ struct mf_op {
   // FP32 copies / scratch for the mixed-precision multigrid (lazily allocated)
   float *metric_f = nullptr, *dinv_f = nullptr, *cd_f = nullptr, *cax_f = nullptr;
   float *r_f = nullptr, *z_f = nullptr;  // mixed-precision Chebyshev-PCG (mf_cg_params.precision = 1)
+  // dev_scal / host_scal (16 doubles): [0..3) dots, [8] p.v, [9] r.r, [10], [11] r.z (ping-pong)
   double *partials = nullptr, *dev_scal = nullptr, *host_scal = nullptr;
+  unsigned *ticket = nullptr;  // last-block counter of the one-pass dot kernels
   double *h_src = nullptr, *h_dst = nullptr;  // device buffers for mf_apply_host
   double *recv_lo = nullptr, *recv_hi = nullptr;
   ncclComm_t comm = nullptr;
@@ -207,8 +209,9 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
     mf_destroy(op);
     return s;
   };
-  if (cudaMallocHost(&op->host_scal, 8 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&op->dev_scal, 8 * sizeof(double)) != cudaSuccess ||
+  if (cudaMallocHost(&op->host_scal, 16 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->dev_scal, 16 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->ticket, sizeof(unsigned)) != cudaSuccess || cudaMemset(op->ticket, 0, sizeof(unsigned)) ||
       cudaMalloc(&op->partials, 3 * kDotBlocks * sizeof(double)) != cudaSuccess)
     return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "scalar buffers"));
 
@@ -262,6 +265,7 @@ extern "C" void mf_destroy(mf_op *op) {
   cudaFree((void *)op->hx.cell_lines);
   cudaFree((void *)op->hx.dir);
   if (op->host_scal) cudaFreeHost(op->host_scal);
+  cudaFree(op->ticket);
   for (cudaEvent_t e : op->ev) cudaEventDestroy(e);
   if (op->comm) ncclCommDestroy(op->comm);
   for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
@@ -392,8 +396,9 @@ extern "C" mf_status mf_create_hex(const mf_hex_mesh *m, int32_t degree, const m
   h.cell_lines = (const uint8_t *)p_cl;
   h.dir = (const int32_t *)p_dir;
   if (!ok) return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "hex mesh arrays"));
-  if (cudaMallocHost(&op->host_scal, 8 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&op->dev_scal, 8 * sizeof(double)) != cudaSuccess ||
+  if (cudaMallocHost(&op->host_scal, 16 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->dev_scal, 16 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&op->ticket, sizeof(unsigned)) != cudaSuccess || cudaMemset(op->ticket, 0, sizeof(unsigned)) ||
       cudaMalloc(&op->partials, 3 * kDotBlocks * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&op->metric, 6 * nc * NV * sizeof(double) + 8) != cudaSuccess)
     return cleanup(fail(MF_ERR_OUT_OF_MEMORY, "scalar / metric buffers"));
@@ -796,13 +801,28 @@ extern "C" mf_status mf_sync(mf_op *op) {
 
 // nd dot products over the owned prefix, summed over ranks; result to host_scal[0..nd)
 static mf_status dots(mf_op *op, int nd, const double *const *a, const double *const *b) {
-  CUDA_TRY(launch_dots(nd, a, b, op->n_owned, op->partials, op->dev_scal, op->stream, &op->launches));
+  CUDA_TRY(launch_dots(nd, a, b, op->n_owned, op->partials, op->ticket, op->dev_scal, op->stream, &op->launches));
   if (op->world > 1) {
     if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
     NCCL_TRY(ncclAllReduce(op->dev_scal, op->dev_scal, nd, ncclDouble, ncclSum, op->comm, op->stream));
   }
   CUDA_TRY(cudaMemcpyAsync(op->host_scal, op->dev_scal, nd * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
   return stream_wait(op);
+}
+
+// a device scalar summed over the ranks, in stream order (no host synchronisation)
+static mf_status allreduce_dev(mf_op *op, double *x, int nd = 1) {
+  if (op->world == 1) return MF_OK;
+  if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
+  NCCL_TRY(ncclAllReduce(x, x, nd, ncclDouble, ncclSum, op->comm, op->stream));
+  return MF_OK;
+}
+
+// out_dev = a.b over the owned prefix, summed over ranks; launched only (stream order)
+mf_status dot_dev(mf_op *op, const double *a, const double *b, double *out_dev) {
+  const double *aa[1] = {a}, *bb[1] = {b};
+  CUDA_TRY(launch_dots(1, aa, bb, op->n_owned, op->partials, op->ticket, out_dev, op->stream, &op->launches));
+  return allreduce_dev(op, out_dev);
 }
 
 // largest eigenvalue of the symmetric tridiagonal (d, e) by Sturm-sequence bisection
@@ -884,8 +904,10 @@ extern "C" mf_status mf_estimate_lambda_max(mf_op *op, int32_t steps, double *la
   return lambda_impl(op, steps, lambda_out);
 }
 
-// O11 / S:648-656: z = Chebyshev(degree) for D^{-1}A on [lam/range, lam] from 0
-static mf_status cheb_impl(mf_op *op, const double *r, double *x, double lam, int degree, double range) {
+// O11 / S:648-656: z = Chebyshev(degree) for D^{-1}A on [lam/range, lam] from 0.  With rz_dev
+// the CG's r.z is formed in the last step's pass (device scalar, summed over ranks).
+static mf_status cheb_impl(mf_op *op, const double *r, double *x, double lam, int degree, double range,
+                           double *rz_dev = nullptr) {
   STATUS_TRY(ensure_solver(op));
   const int64_t n = op->n_local;
   const double a = lam / range, b = lam;
@@ -895,10 +917,17 @@ static mf_status cheb_impl(mf_op *op, const double *r, double *x, double lam, in
   for (int j = 1; j < degree; ++j) {
     const double rho_n = 1.0 / (2.0 * sigma - rho);
     STATUS_TRY(apply_impl(op, x, op->cax));
+    if (rz_dev && j == degree - 1) {
+      CUDA_TRY(launch_cheb_step_rz(r, op->cax, op->dinv, rho_n * rho, 2.0 * rho_n / delta, x, op->cd, n,
+                                   op->n_owned, op->partials, op->ticket, rz_dev, op->stream, &op->launches));
+      STATUS_TRY(allreduce_dev(op, rz_dev));
+      return MF_OK;
+    }
     CUDA_TRY(launch_cheb_step(r, op->cax, op->dinv, rho_n * rho, 2.0 * rho_n / delta, x, op->cd, n, op->stream,
                               &op->launches));
     rho = rho_n;
   }
+  if (rz_dev) STATUS_TRY(dot_dev(op, r, x, rz_dev));
   return MF_OK;
 }
 
@@ -970,12 +999,19 @@ extern "C" mf_status mf_apply_f32(mf_op *op, const float *src, int64_t n_src, fl
 // buffers of n_local); stopping rule, history and errors of mf_cg_solve.  Also the
 // outer loop of the multigrid solver (mg.cu).
 mf_status cg_core(mf_op *op, const double *b, double *x, double rel_tol, int max_iter,
-                  const std::function<mf_status(const double *, double *)> &precond, mf_cg_result *res,
+                  const std::function<mf_status(const double *, double *, double *)> &precond, mf_cg_result *res,
                   double *history, int32_t history_cap) {
+  // One host synchronisation per iteration: alpha = (r.z)/(p.v) and beta = (r.z)'/(r.z) are
+  // formed on the device by the update kernels, r.r is fused into the x / r update and r.z
+  // into the preconditioner's last pass (precond(r, z, rz_dev) stores it); the host then
+  // reads p.v, r.r and r.z together for the stopping test and the breakdown checks.  The
+  // preconditioner of the final iteration runs before the test that ends the loop (unused).
+  // Same arithmetic and reduction order as the host-scalar loop, so the same iterates.
   STATUS_TRY(ensure_solver(op));
   const int64_t n = op->n_local;
   cudaStream_t s = op->stream;
   double *r = op->r, *p = op->p, *v = op->v, *z = op->z;
+  double *PV = op->dev_scal + 8, *RR = op->dev_scal + 9, *RZ[2] = {op->dev_scal + 10, op->dev_scal + 11};
   res->iterations = 0;
   res->final_rel_residual = 0.0;
   CUDA_TRY(launch_zero(x, n, s, &op->launches));
@@ -986,50 +1022,31 @@ mf_status cg_core(mf_op *op, const double *b, double *x, double rel_tol, int max
   }
   const double normb = std::sqrt(op->host_scal[0]);
   if (normb == 0.0) return MF_OK;
-  STATUS_TRY(precond(r, z));
+  int cur = 0;
+  STATUS_TRY(precond(r, z, RZ[cur]));
   CUDA_TRY(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  {
-    const double *a[1] = {r}, *bb[1] = {z};
-    STATUS_TRY(dots(op, 1, a, bb));
-  }
-  double rz = op->host_scal[0];
   int it = 0;
   while (true) {
     STATUS_TRY(apply_impl(op, p, v));
     ++it;
-    {
-      const double *a[1] = {p}, *bb[1] = {v};
-      STATUS_TRY(dots(op, 1, a, bb));
-    }
-    const double pv = op->host_scal[0];
-    if (!(pv > 0.0)) {
-      res->iterations = it;
-      return fail(MF_ERR_BREAKDOWN, "p.Ap <= 0");
-    }
-    op->host_scal[4] = rz / pv;
-    CUDA_TRY(cudaMemcpyAsync(op->dev_scal + 4, op->host_scal + 4, sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(launch_cg_update_xr(op->dev_scal + 4, x, r, p, v, n, s, &op->launches));
-    {
-      const double *a[1] = {r}, *bb[1] = {r};
-      STATUS_TRY(dots(op, 1, a, bb));
-    }
-    const double resn = std::sqrt(op->host_scal[0]);
-    if (history && it <= history_cap) history[it - 1] = resn;
+    STATUS_TRY(dot_dev(op, p, v, PV));
+    CUDA_TRY(launch_cg_xr_rr(RZ[cur], PV, x, r, p, v, n, op->n_owned, op->partials, op->ticket, RR, s,
+                             &op->launches));
+    STATUS_TRY(allreduce_dev(op, RR));
+    STATUS_TRY(precond(r, z, RZ[cur ^ 1]));
+    CUDA_TRY(cudaMemcpyAsync(op->host_scal + 8, op->dev_scal + 8, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    STATUS_TRY(stream_wait(op));
+    const double pv = op->host_scal[8], rr = op->host_scal[9], rzn = op->host_scal[10 + (cur ^ 1)];
     res->iterations = it;
+    if (!(pv > 0.0)) return fail(MF_ERR_BREAKDOWN, "p.Ap <= 0");
+    const double resn = std::sqrt(rr);
+    if (history && it <= history_cap) history[it - 1] = resn;
     res->final_rel_residual = resn / normb;
     if (resn <= rel_tol * normb) return MF_OK;
     if (it >= max_iter) return fail(MF_ERR_MAX_ITERATIONS, "CG did not converge");
-    STATUS_TRY(precond(r, z));
-    {
-      const double *a[1] = {r}, *bb[1] = {z};
-      STATUS_TRY(dots(op, 1, a, bb));
-    }
-    const double rzn = op->host_scal[0];
     if (!(rzn > 0.0)) return fail(MF_ERR_BREAKDOWN, "r.z <= 0");
-    op->host_scal[5] = rzn / rz;
-    CUDA_TRY(cudaMemcpyAsync(op->dev_scal + 5, op->host_scal + 5, sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(launch_cg_update_p(op->dev_scal + 5, z, p, n, s, &op->launches));
-    rz = rzn;
+    CUDA_TRY(launch_cg_p_dev(RZ[cur ^ 1], RZ[cur], z, p, n, s, &op->launches));
+    cur ^= 1;
   }
 }
 
@@ -1059,16 +1076,16 @@ extern "C" mf_status mf_cg_solve(mf_op *op, const double *b, double *x, int64_t 
       CUDA_TRY(cudaMalloc(&op->z_f, n * sizeof(float)));
     }
   }
-  auto precond = [&](const double *rr, double *zz) -> mf_status {
+  auto precond = [&](const double *rr, double *zz, double *rz_dev) -> mf_status {
     if (mixed) {  // z = P(r) in FP32: round r, run the same Chebyshev recurrence, widen z
       CUDA_TRY(launch_d2f(rr, op->r_f, n, op->stream, &op->launches));
       STATUS_TRY(cheb_f32(op, op->r_f, op->z_f, lam, prm->cheb_degree, prm->cheb_range));
       CUDA_TRY(launch_f2d(op->z_f, zz, n, op->stream, &op->launches));
-      return MF_OK;
+      return dot_dev(op, rr, zz, rz_dev);
     }
-    if (prm->cheb_degree > 0) return cheb_impl(op, rr, zz, lam, prm->cheb_degree, prm->cheb_range);
+    if (prm->cheb_degree > 0) return cheb_impl(op, rr, zz, lam, prm->cheb_degree, prm->cheb_range, rz_dev);
     CUDA_TRY(launch_mul(op->dinv, rr, zz, n, op->stream, &op->launches));
-    return MF_OK;
+    return dot_dev(op, rr, zz, rz_dev);
   };
   return cg_core(op, b, x, prm->rel_tol, prm->max_iter, precond, res, history, history_cap);
 }

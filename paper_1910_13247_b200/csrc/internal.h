@@ -110,18 +110,22 @@ cudaError_t launch_set_constrained(const Geo &g, double *x, double value, cudaSt
 // vector kernels (kernels_vec.cu)
 cudaError_t launch_splitmix(double *x, int64_t n, int64_t first_global, uint64_t seed, cudaStream_t s,
                             int64_t *launches);
-// partial dot products into `partials` (fixed block count), then a second pass into out[j]
+// nd dot products in one pass (fixed block count, last block reduces in block order) into
+// out[0..nd); partials: 3 kDotBlocks doubles, ticket: a zeroed device counter
 cudaError_t launch_dots(int ndots, const double *const *a, const double *const *b, int64_t n,
-                        double *partials, double *out, cudaStream_t s, int64_t *launches);
+                        double *partials, unsigned *ticket, double *out, cudaStream_t s, int64_t *launches);
+// fused CG / Chebyshev steps with the step lengths on the device and the next dot in the same pass
+cudaError_t launch_cg_xr_rr(const double *rz, const double *pv, double *x, double *r, const double *p,
+                            const double *v, int64_t n, int64_t n_owned, double *partials, unsigned *ticket,
+                            double *rr, cudaStream_t s, int64_t *launches);
+cudaError_t launch_cg_p_dev(const double *rz_new, const double *rz_old, const double *z, double *p, int64_t n,
+                            cudaStream_t s, int64_t *launches);
+cudaError_t launch_cheb_step_rz(const double *r, const double *ax, const double *dinv, double c1, double c2,
+                                double *x, double *d, int64_t n, int64_t n_owned, double *partials,
+                                unsigned *ticket, double *rz, cudaStream_t s, int64_t *launches);
 // y = a*x + b*y   (and variants used by CG / Chebyshev)
 cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n, cudaStream_t s,
                          int64_t *launches);
-// CG update with device scalars: alpha = num/den -> x += alpha p, r -= alpha v
-cudaError_t launch_cg_update_xr(const double *scal, double *x, double *r, const double *p, const double *v,
-                                int64_t n, cudaStream_t s, int64_t *launches);
-// p = z + beta p, beta = scal
-cudaError_t launch_cg_update_p(const double *beta, const double *z, double *p, int64_t n, cudaStream_t s,
-                               int64_t *launches);
 // Chebyshev: first step x = dinv*r*c0 (d = x), later d = c1*d + c2*dinv*(r - Ax); x += d
 cudaError_t launch_cheb_init(const double *r, const double *dinv, double c0, double *x, double *d, int64_t n,
                              cudaStream_t s, int64_t *launches);
@@ -171,9 +175,11 @@ constexpr int kDotBlocks = 592;  // 4 x 148 SMs
 }  // namespace mf
 
 // api.cu internals shared with mg.cu (C++ linkage, not part of the C ABI)
+// precond(r, z, rz_dev): z = P r and rz_dev = r.z (device scalar, summed over ranks)
 mf_status cg_core(mf_op *op, const double *b, double *x, double rel_tol, int max_iter,
-                  const std::function<mf_status(const double *, double *)> &precond, mf_cg_result *res,
+                  const std::function<mf_status(const double *, double *, double *)> &precond, mf_cg_result *res,
                   double *history, int32_t history_cap);
+mf_status dot_dev(mf_op *op, const double *a, const double *b, double *out_dev);
 mf_status mf_set_error(mf_status s, const std::string &msg);  // sets mf_last_error, returns s
 // FP32 operator and Chebyshev polynomial of an op (3D, one rank)
 mf_status apply_f32(mf_op *op, const float *src, float *dst);

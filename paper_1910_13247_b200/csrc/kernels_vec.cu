@@ -52,16 +52,14 @@ struct DotArgs {
   const double *b[3];
 };
 
+// Dot products in ONE pass (fixed block count kDotBlocks, grid-stride): each block sums its
+// products (per-thread FMA, then a warp / block tree), writes its partial, and the last block
+// to finish (atomic ticket) adds the partials in block order and stores the result -- a
+// deterministic order, no second launch.  The same tail finishes the fused update kernels.
 template <int ND>
-__global__ void __launch_bounds__(256) k_dot_partial(DotArgs args, int64_t n, double *partials) {
-  double acc[ND];
-#pragma unroll
-  for (int j = 0; j < ND; ++j) acc[j] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-    for (int j = 0; j < ND; ++j) acc[j] = fma(args.a[j][i], args.b[j][i], acc[j]);
-  }
+__device__ __forceinline__ void dot_finish(const double (&acc)[ND], double *partials, unsigned *ticket, double *out) {
   __shared__ double red[ND][8];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < ND; ++j) {
@@ -74,31 +72,114 @@ __global__ void __launch_bounds__(256) k_dot_partial(DotArgs args, int64_t n, do
     double s = 0.0;
     for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
     partials[threadIdx.x * kDotBlocks + blockIdx.x] = s;
+    __threadfence();
   }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (wid < ND) {
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partials + wid * kDotBlocks + b);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[wid] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch (stream order)
 }
 
-__global__ void k_dot_final(const double *partials, int nd, double *out) {
-  // one warp per dot, fixed order: deterministic
-  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (j >= nd) return;
-  double s = 0.0;
-  for (int b = lane; b < kDotBlocks; b += 32) s += partials[j * kDotBlocks + b];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[j] = s;
+template <int ND>
+__global__ void __launch_bounds__(256) k_dot(DotArgs args, int64_t n, double *partials, unsigned *ticket,
+                                             double *out) {
+  double acc[ND];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) acc[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) acc[j] = fma(args.a[j][i], args.b[j][i], acc[j]);
+  }
+  dot_finish<ND>(acc, partials, ticket, out);
 }
 
 cudaError_t launch_dots(int nd, const double *const *a, const double *const *b, int64_t n, double *partials,
-                        double *out, cudaStream_t s, int64_t *launches) {
+                        unsigned *ticket, double *out, cudaStream_t s, int64_t *launches) {
   DotArgs args{};
   for (int j = 0; j < nd; ++j) {
     args.a[j] = a[j];
     args.b[j] = b[j];
   }
-  *launches += 2;
-  if (nd == 1) k_dot_partial<1><<<kDotBlocks, 256, 0, s>>>(args, n, partials);
-  else if (nd == 2) k_dot_partial<2><<<kDotBlocks, 256, 0, s>>>(args, n, partials);
-  else k_dot_partial<3><<<kDotBlocks, 256, 0, s>>>(args, n, partials);
-  k_dot_final<<<1, 32 * nd, 0, s>>>(partials, nd, out);
+  ++*launches;
+  if (nd == 1) k_dot<1><<<kDotBlocks, 256, 0, s>>>(args, n, partials, ticket, out);
+  else if (nd == 2) k_dot<2><<<kDotBlocks, 256, 0, s>>>(args, n, partials, ticket, out);
+  else k_dot<3><<<kDotBlocks, 256, 0, s>>>(args, n, partials, ticket, out);
+  return cudaGetLastError();
+}
+
+// CG update with the step length on the device: alpha = sc[rz] / sc[pv];
+// x += alpha p, r -= alpha v, and rr = r.r over the owned prefix, in one pass
+__global__ void __launch_bounds__(256) k_cg_xr_rr(const double *__restrict__ rz, const double *__restrict__ pv,
+                                                  double *__restrict__ x, double *__restrict__ r,
+                                                  const double *__restrict__ p, const double *__restrict__ v,
+                                                  int64_t n, int64_t n_owned, double *partials, unsigned *ticket,
+                                                  double *rr) {
+  const double alpha = rz[0] / pv[0];
+  double acc[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, v[i], r[i]);
+    r[i] = ri;
+    if (i < n_owned) acc[0] = fma(ri, ri, acc[0]);
+  }
+  dot_finish<1>(acc, partials, ticket, rr);
+}
+
+cudaError_t launch_cg_xr_rr(const double *rz, const double *pv, double *x, double *r, const double *p,
+                            const double *v, int64_t n, int64_t n_owned, double *partials, unsigned *ticket,
+                            double *rr, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cg_xr_rr<<<kDotBlocks, 256, 0, s>>>(rz, pv, x, r, p, v, n, n_owned, partials, ticket, rr);
+  return cudaGetLastError();
+}
+
+// beta = rz_new / rz_old on the device; p = z + beta p
+__global__ void k_cg_p_dev(const double *__restrict__ rz_new, const double *__restrict__ rz_old,
+                           const double *__restrict__ z, double *__restrict__ p, int64_t n) {
+  const double b = rz_new[0] / rz_old[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], z[i]);
+}
+
+cudaError_t launch_cg_p_dev(const double *rz_new, const double *rz_old, const double *z, double *p, int64_t n,
+                            cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cg_p_dev<<<grid_for(n), 256, 0, s>>>(rz_new, rz_old, z, p, n);
+  return cudaGetLastError();
+}
+
+// the last Chebyshev step with the CG's r.z fused: d = c1 d + c2 dinv (r - ax);
+// x += d; rz = r.x over the owned prefix
+__global__ void __launch_bounds__(256) k_cheb_step_rz(const double *__restrict__ r, const double *__restrict__ ax,
+                                                      const double *__restrict__ dinv, double c1, double c2,
+                                                      double *__restrict__ x, double *__restrict__ d, int64_t n,
+                                                      int64_t n_owned, double *partials, unsigned *ticket,
+                                                      double *rz) {
+  double acc[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = r[i];
+    const double dn = c1 * d[i] + c2 * (dinv[i] * (ri - ax[i]));
+    d[i] = dn;
+    const double xn = x[i] + dn;
+    x[i] = xn;
+    if (i < n_owned) acc[0] = fma(ri, xn, acc[0]);
+  }
+  dot_finish<1>(acc, partials, ticket, rz);
+}
+
+cudaError_t launch_cheb_step_rz(const double *r, const double *ax, const double *dinv, double c1, double c2,
+                                double *x, double *d, int64_t n, int64_t n_owned, double *partials,
+                                unsigned *ticket, double *rz, cudaStream_t s, int64_t *launches) {
+  ++*launches;
+  k_cheb_step_rz<<<kDotBlocks, 256, 0, s>>>(r, ax, dinv, c1, c2, x, d, n, n_owned, partials, ticket, rz);
   return cudaGetLastError();
 }
 
@@ -111,37 +192,6 @@ cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t
                          int64_t *launches) {
   ++*launches;
   k_axpby<<<grid_for(n), 256, 0, s>>>(a, x, b, y, n);
-  return cudaGetLastError();
-}
-
-// scal[0] = alpha: x += alpha p; r -= alpha v
-__global__ void k_cg_xr(const double *__restrict__ scal, double *__restrict__ x, double *__restrict__ r,
-                        const double *__restrict__ p, const double *__restrict__ v, int64_t n) {
-  const double alpha = scal[0];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] = fma(alpha, p[i], x[i]);
-    r[i] = fma(-alpha, v[i], r[i]);
-  }
-}
-
-cudaError_t launch_cg_update_xr(const double *scal, double *x, double *r, const double *p, const double *v,
-                                int64_t n, cudaStream_t s, int64_t *launches) {
-  ++*launches;
-  k_cg_xr<<<grid_for(n), 256, 0, s>>>(scal, x, r, p, v, n);
-  return cudaGetLastError();
-}
-
-__global__ void k_cg_p(const double *__restrict__ beta, const double *__restrict__ z, double *__restrict__ p,
-                       int64_t n) {
-  const double b = beta[0];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(b, p[i], z[i]);
-}
-
-cudaError_t launch_cg_update_p(const double *beta, const double *z, double *p, int64_t n, cudaStream_t s,
-                               int64_t *launches) {
-  ++*launches;
-  k_cg_p<<<grid_for(n), 256, 0, s>>>(beta, z, p, n);
   return cudaGetLastError();
 }
 

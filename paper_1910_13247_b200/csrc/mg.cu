@@ -547,7 +547,10 @@ extern "C" mf_status mf_mg_cg_solve(mf_mg *mg, const double *b, double *x, int64
   if (n != mg->n[mg->L - 1]) return mf_set_error(MF_ERR_LENGTH, "vector length != finest n_local");
   if (!(rel_tol > 0.0) || max_iter < 1) return mf_set_error(MF_ERR_ARGUMENT, "bad CG parameters");
   result->lambda_max = mg->lam[mg->L - 1];
-  auto precond = [&](const double *r, double *z) -> mf_status { return vcycle_top(mg, r, z); };
+  auto precond = [&](const double *r, double *z, double *rz_dev) -> mf_status {
+    const mf_status st = vcycle_top(mg, r, z);
+    return st != MF_OK ? st : dot_dev(mg->ops[mg->L - 1], r, z, rz_dev);
+  };
   return cg_core(mg->ops[mg->L - 1], b, x, rel_tol, max_iter, precond, result, history, history_cap);
 }
 
