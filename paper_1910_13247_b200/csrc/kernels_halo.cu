@@ -112,6 +112,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// MF_CHECKED builds trap on any out-of-range global / shared / distributed-shared index (the
+// compute-sanitizer substitute: it is closed on this GPU pool)
+#ifdef MF_CHECKED
+#define HCHECK(c)          \
+  do {                     \
+    if (!(c)) __trap();    \
+  } while (0)
+#else
+#define HCHECK(c) \
+  do {            \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void split5(const double *u, double *e, double *o) {
   e[0] = u[0] + u[4];
   e[1] = u[1] + u[3];
@@ -303,6 +316,10 @@ __global__ void __launch_bounds__(HNT, 1)
         const int64_t gz = plane_of(t);
         const double *s0 = src + gz * plane + (y0 - HK) * Nx + gx;
         double *st = US + (t % NS) * US_STAGE + yt;
+#ifdef MF_CHECKED
+        for (int i = 0; i < HYR; ++i)
+          if ((inmask >> i) & 1u) HCHECK(s0 + i * Nx >= src && s0 + i * Nx < src + plane * Nz);
+#endif
         if (allin) {
 #pragma unroll
           for (int i = 0; i < HYR; ++i) cp_async_z<double>(st + i * 32 * HROWS, s0 + i * Nx, 8u);
@@ -316,7 +333,10 @@ __global__ void __launch_bounds__(HNT, 1)
           double *c = C128 + (gz % C128_RING) * (HROWS + 1);
 #pragma unroll
           for (int r = 0; r <= HROWS; ++r)
-            if (r < nrow) cp_async_z<double>(c + r, s1 + r * Nx, 8u);
+            if (r < nrow) {
+              HCHECK(s1 + r * Nx >= src && s1 + r * Nx < src + plane * Nz);
+              cp_async_z<double>(c + r, s1 + r * Nx, 8u);
+            }
         }
 #endif
       }
@@ -353,8 +373,10 @@ __global__ void __launch_bounds__(HNT, 1)
             double *d0 = dst + gz * plane + y0 * Nx + gx;
 #pragma unroll
             for (int r = 0; r <= HROWS; ++r)
-              if (r < nrow && yc < ncol && (zc || colc || ((consmask >> (r + HK)) & 1u)))
+              if (r < nrow && yc < ncol && (zc || colc || ((consmask >> (r + HK)) & 1u))) {
+                HCHECK(d0 + r * Nx >= dst && d0 + r * Nx < dst + plane * Nz);
                 d0[r * Nx] = skipid ? 0.0 : u[r + HK];
+              }
           }
           if (zc || colc || !colin) {
 #pragma unroll
@@ -423,6 +445,7 @@ __global__ void __launch_bounds__(HNT, 1)
       if (on) {
         double *pa = AB + b * AB_BUF + yj * AB_PL + hxs(yc);
         double *pb = pa + 2 * AB_PL;
+        HCHECK(pb + (HROWS - 1) * HXP < AB + NB * AB_BUF);
 #pragma unroll
         for (int r = 0; r < HROWS; ++r) {
           pa[r * HXP] = av[r];
@@ -431,6 +454,7 @@ __global__ void __launch_bounds__(HNT, 1)
         if (yc == 0 && rank > 0) {  // column 0 -> the left CTA's column-128 slot of this step
           const int sc = t % DCOL;
           double *cs = COL + sc * COL_SLOT + yj * 2 * HROWS;
+          HCHECK(cs + 2 * HROWS <= COL + DCOL * COL_SLOT);
 #pragma unroll
           for (int r = 0; r < HROWS; r += 2) {
             st_async2(cs + r, b_col + 8 * sc, rank - 1, av[r], av[r + 1]);
@@ -472,6 +496,8 @@ __global__ void __launch_bounds__(HNT, 1)
         bb[i] = pb[xb + i];
       }
       const double *pa4 = lane == 31 ? c : pa + xb4, *pb4 = lane == 31 ? c + HROWS : pb + xb4;
+      HCHECK(pb + xb < AB + NB * AB_BUF && ((lane == 31 && pb4 < COL + DCOL * COL_SLOT) ||
+                                            (lane < 31 && pb4 < AB + NB * AB_BUF)));
       a[HK] = *pa4;
       bb[HK] = *pb4;
       double ea[3], oa[2], eb[3], ob[2], ve[3], vo[2];
@@ -496,6 +522,7 @@ __global__ void __launch_bounds__(HNT, 1)
       }
       if (lane == 31 && !last_x) {
         const int s = (L - Ls) % DHL;
+        HCHECK(s >= 0 && (m * HROWS + w) * 2 + 1 < HL_SLOT);
         st_async2(HL + s * HL_SLOT + (m * HROWS + w) * 2, b_hl + 8 * s, rank + 1, Pv[HK], Qv[HK]);
       }
     };
@@ -511,9 +538,11 @@ __global__ void __launch_bounds__(HNT, 1)
         for (int l = 0; l < np; ++l) {
           const int64_t gz = gz0 + l;
           double *const drow = dst + gz * plane + y * Nx + x0 + lane;
+          HCHECK(gz >= 0 && gz < Nz && y < Ny);
           if (c128) {
             const double *c = C128 + (gz % C128_RING) * (HROWS + 1);
             const bool skipid = P.skip_top_identity && gz == Nz - 1;
+            HCHECK(drow + HCOLS < dst + plane * Nz);
             drow[HCOLS] = skipid ? 0.0 : c[w];
             if (w == 0 && nrow > HROWS) drow[HROWS * Nx + HCOLS] = skipid ? 0.0 : c[HROWS];
           }
