@@ -274,3 +274,18 @@ def test_rhs_constant_sums_to_free_integral():
     for geom in (0, 1):
         p = oracle.problem(dim=3, n_cells=(3, 3, 3), degree=3, geom=geom, dirichlet=0)
         assert abs(oracle.rhs(p, 0).sum() - 1.0) < 1e-13
+
+
+@pytest.mark.parametrize("geom,coeff_kind,k", [(0, 0, 1), (0, 0, 3), (1, 1, 2), (1, 1, 4)])
+def test_csr_diagonal_equals_dense_diagonal_on_free_rows(geom, coeff_kind, k):
+    # CSR.diagonal() (the a9 reference of the GPU diagonal) is the diagonal of the assembled
+    # matrix itself (Eq. (1)): compare with diag(dense()) on the free rows, where the
+    # entries come from the quadrature, and on the constrained rows (identity, R3)
+    p = oracle.problem(dim=3, n_cells=(3, 2, 2), degree=k, geom=geom, coeff_kind=coeff_kind)
+    A = oracle.CSR(p)
+    m = oracle.constrained_mask_fast(p)
+    d, D = A.diagonal(), np.diag(A.dense())
+    assert (~m).sum() > 0
+    np.testing.assert_array_equal(d[~m], D[~m])
+    np.testing.assert_array_equal(d[m], 1.0)
+    assert np.all(d[~m] > 0)
