@@ -48,13 +48,28 @@ CONFIGS = {
 METRIC = "DoFs/s per matrix-free Laplace apply (3D Q_k FP64)"
 
 
-def load_traffic(config):
-    """ncu-measured DRAM bytes per launch of the timed region (profiles/traffic.json), or None."""
+def lib_build():
+    """sha1 (12 hex) of the library this run loads (matches profiles/traffic.json "build")."""
+    import hashlib
+
+    from paper_1910_13247_b200 import build as _b
+
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f)[config]["bytes_per_launch"]
+        with open(os.environ.get("MF_LIB_PATH") or _b.LIB, "rb") as f:
+            return hashlib.sha1(f.read()).hexdigest()[:12]
     except Exception:
         return None
+
+
+def load_traffic(config):
+    """ncu-measured DRAM bytes per launch of the timed region (profiles/traffic.json) with the
+    profile files and the build they came from, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            e = json.load(f)[config]
+        return e["bytes_per_launch"], {"source": e.get("source"), "build": e.get("build")}
+    except Exception:
+        return None, None
 
 
 FP64_PEAK_TINSTR = 57.47 * 148 * 1.965e9 / 1e12  # measured DFMA issue rate (profiles/r01_microbench.json)
@@ -70,7 +85,7 @@ def fp64_roofline(config, n_dofs, kernel_ms):
         return None
     achieved = ipd * n_dofs / (kernel_ms * 1e-3) / 1e12
     return {"instr_per_dof": ipd, "achieved": achieved, "peak": FP64_PEAK_TINSTR, "unit": "T FP64 instr/s",
-            "frac": achieved / FP64_PEAK_TINSTR}
+            "frac": achieved / FP64_PEAK_TINSTR, "t_min_ms": ipd * n_dofs / (FP64_PEAK_TINSTR * 1e12) * 1e3}
 
 
 def load_peaks():
@@ -439,6 +454,15 @@ def main():
         peak, peak_kind = load_peaks()
         bytes_per_launch = info1["bytes_algorithmic"]
         achieved = bytes_per_launch / (kern_avg_ms * 1e-3) / 1e9
+        traffic, traffic_src = load_traffic(args.config)
+        build = lib_build()
+        fp64 = fp64_roofline(args.config, op.n_local, kern_avg_ms)
+        # the binding roof: the larger of the HBM time of the algorithmic bytes and the FP64 time of
+        # the counted instructions; frac below stays the north star's % of HBM
+        t_hbm = bytes_per_launch / (peak * 1e9) * 1e3
+        binding = {"hbm_min_ms": t_hbm, "fp64_min_ms": fp64["t_min_ms"] if fp64 else None,
+                   "roof": "hbm" if not fp64 or t_hbm >= fp64["t_min_ms"] else "fp64",
+                   "frac_of_binding": max(t_hbm, fp64["t_min_ms"] if fp64 else 0.0) / kern_avg_ms}
         out = {
             "metric": METRIC, "value": value, "unit": "DoFs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -449,10 +473,11 @@ def main():
                        "apply_variant": info1["apply_variant"],
                        "l2": f"inputs larger than L2: {info1['bytes_algorithmic'] / 1e6:.0f} MB streamed per apply (src, dst, stored metric / indices) > 126 MB"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": load_traffic(args.config), "peak_kind": peak_kind,
-                         "bytes_per_launch": bytes_per_launch, "kernel_ms": kern_avg_ms,
-                         "kernel_share_of_step": kern_avg_ms / ms_per_step,
-                         "fp64": fp64_roofline(args.config, op.n_local, kern_avg_ms)},
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "traffic_source": traffic_src,
+                         "traffic_build_matches": bool(traffic_src and build and traffic_src.get("build") == build),
+                         "build": build, "bytes_per_launch": bytes_per_launch, "kernel_ms": kern_avg_ms,
+                         "kernel_share_of_step": kern_avg_ms / ms_per_step, "fp64": fp64, "binding": binding},
             "e2e": {"value": e2e_val, "unit": "DoFs/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "steps": e2e_steps},
             "gpu_launches": launches,
