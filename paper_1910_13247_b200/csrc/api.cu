@@ -459,9 +459,10 @@ static int chosen_variant(const mf_op *op) {
 extern "C" mf_status mf_set_apply_variant(mf_op *op, int32_t variant) {
   if (!op) return fail(MF_ERR_ARGUMENT, "null op");
   if (op->hex || op->dg) return fail(MF_ERR_ARGUMENT, "DG / hex operators have one kernel family");
-  if ((variant == kVariantCartTile && !cart_tile_supported(op->g)) ||
-      (variant == kVariantCartPlane && !cart_plane_supported(op->g)))
-    return fail(MF_ERR_ARGUMENT, "tile/plane kernels need dim 3, Cartesian geometry, constant coefficient, k 2..4");
+  if (variant == kVariantCartTile)
+    return fail(MF_ERR_ARGUMENT, "variant 2 (the slab-form tile kernel) was removed: use 3 (plane) or 6 (halo)");
+  if (variant == kVariantCartPlane && !cart_plane_supported(op->g))
+    return fail(MF_ERR_ARGUMENT, "the plane kernel needs dim 3, Cartesian geometry, constant coefficient, k 2..4");
   if (variant == kVariantCartHalo && !cart_halo_supported(op->g))
     return fail(MF_ERR_ARGUMENT,
                 "halo kernel needs dim 3, Cartesian, constant coefficient, k 4, n_cells x <= 256, and Dirichlet "
@@ -558,7 +559,6 @@ extern "C" mf_status mf_apply_split_part(mf_op *op, const double *src, int64_t n
   if (op->hex || op->dg || op->g.dim != 3 || (part != 1 && part != 2))
     return fail(MF_ERR_ARGUMENT, "split parts: 3D brick operator, part 1 or 2");
   const int var = chosen_variant(op);
-  if (var == kVariantCartTile) return fail(MF_ERR_ARGUMENT, "the tile variant has no split");
   if (var == kVariantCartHalo) {
     CUDA_TRY(launch_apply_cart_halo(op->g, op->t, src, dst, op->stream, &op->launches, part));
   } else if (var == kVariantCartPlane) {
@@ -583,12 +583,8 @@ static mf_status apply_impl(mf_op *op, const double *src, double *dst) {
     return timing_mark(op);
   }
   const int var = chosen_variant(op);
-  if (op->zsplit && op->g.dim == 3 && var != kVariantCartTile) return apply_split(op, src, dst, var);
-  if (var == kVariantCartTile) {
-    STATUS_TRY(timing_mark(op));
-    CUDA_TRY(launch_apply_cart_tile(op->g, op->t, src, dst, op->stream, &op->launches));
-    STATUS_TRY(timing_mark(op));
-  } else if (var == kVariantCartHalo) {
+  if (op->zsplit && op->g.dim == 3) return apply_split(op, src, dst, var);
+  if (var == kVariantCartHalo) {
     STATUS_TRY(timing_mark(op));
     CUDA_TRY(launch_apply_cart_halo(op->g, op->t, src, dst, op->stream, &op->launches));
     STATUS_TRY(timing_mark(op));

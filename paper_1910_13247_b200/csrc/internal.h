@@ -58,7 +58,7 @@ struct Geo {
 enum Variant {
   kVariantAuto = 0,
   kVariantGeneral = 1,  // 12-sweep collocation kernel, any dim/k/geometry
-  kVariantCartTile = 2, // Cartesian constant-coefficient 3D tile kernel (slab form)
+  kVariantCartTile = 2, // (removed in r02: the slab-form tile kernel, slower than the plane kernel)
   kVariantCartPlane = 3, // Cartesian constant-coefficient 3D, 2D-first / z-last form
   kVariantDG = 4,        // mf_create_dg (reported by mf_get_info)
   kVariantHex = 5,       // mf_create_hex (reported by mf_get_info)
@@ -71,9 +71,6 @@ enum Variant {
 // (part 1 then part 2 = part 0).  The 2D and tile paths take part 0 only.
 cudaError_t launch_apply_general(const Geo &g, const Tables &t, const double *src, double *dst,
                                  const double *metric, cudaStream_t s, int64_t *launches, int part = 0);
-cudaError_t launch_apply_cart_tile(const Geo &g, const Tables &t, const double *src, double *dst,
-                                   cudaStream_t s, int64_t *launches);
-bool cart_tile_supported(const Geo &g);
 cudaError_t launch_apply_cart_plane(const Geo &g, const Tables &t, const double *src, double *dst,
                                     cudaStream_t s, int64_t *launches, int part = 0);
 // FP32 versions for the mixed-precision multigrid (§8(f) f2): the same kernels

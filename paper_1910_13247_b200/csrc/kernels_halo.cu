@@ -59,8 +59,7 @@ constexpr int HMAXCH = 64;                 // z-chunks per launch
 constexpr int HMAXCLU = 8;                 // portable cluster size -> n_cells x <= 256
 constexpr int NB = 3;                      // a/b buffers (producer lead)
 constexpr int NS = 3;                      // producer input stages (cp.async ring: 2 steps of prefetch)
-constexpr int PROD_REGS = 104, CONS_REGS = 152;
-constexpr int PFD = 0;                     // L2 prefetch distance beyond the staged steps (0: off)  // per-role register budgets (setmaxnreg; sum 256 = 2 x 128)
+constexpr int PROD_REGS = 104, CONS_REGS = 152;  // per-role register budgets (setmaxnreg; sum 256 = 2 x 128)
 // Column-128 slots (written by the right CTA's producers) and x-halo slots (written by the
 // left CTA's consumers, one per layer).  The right CTA's producer reaches step t + DCOL only
 // after its consumers finished step t + DCOL - NB, whose node-0 completion waited for this
@@ -162,12 +161,6 @@ __device__ __forceinline__ unsigned map_rank(unsigned a, int rank) {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-// named hardware barriers for the intra-CTA producer / consumer hand-off (waiting warps sleep
-// instead of polling): ids 1..NB = buffer full, NB+1..2NB = buffer empty; all 512 threads count
-__device__ __forceinline__ void nb_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "n"(HNT) : "memory");
-}
-__device__ __forceinline__ void nb_sync(int id) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(HNT) : "memory"); }
 __device__ __forceinline__ void bar_init(unsigned a, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
 }

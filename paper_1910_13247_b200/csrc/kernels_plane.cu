@@ -2,7 +2,7 @@
 // form (apply variant 3, the default for k = 2..4).
 //
 // The cell operator of the affine box cell is the Gauss(k+1)-exact Kronecker form
-// (see kernels_tile.cu)
+//
 //     A_c = [Kx' (x) My + Mx (x) Ky'] (x) Mz  +  [Mx (x) My] (x) Kz'     (x, y | z)
 // so with the x-y operators applied on every DoF plane p and summed over the
 // cells that share a node in x-y,
@@ -431,7 +431,10 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T
   return cudaLaunchKernelEx(&cfg, k_apply_plane<K, TX, TY, ISO, T>, P, src, dst);
 }
 
-bool cart_plane_supported(const Geo &g) { return cart_tile_supported(g); }
+bool cart_plane_supported(const Geo &g) {
+  return g.dim == 3 && g.geom == MF_GEOM_CARTESIAN && g.coeff_kind == MF_COEFF_CONSTANT &&
+         (g.k == 2 || g.k == 3 || g.k == 4);
+}
 
 // k = 4 tiles: 16 x 2 cells by default -- 3 instead of 7 strided x tile-edge planes in
 // the init on 64^3 (its y-edge planes are contiguous rows); cfg 3 168.0 vs 173.9 us per

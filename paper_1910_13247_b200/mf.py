@@ -19,7 +19,7 @@ STATUS = {
     -5: "MF_ERR_BREAKDOWN", -6: "MF_ERR_CUDA", -7: "MF_ERR_NCCL", -8: "MF_ERR_OUT_OF_MEMORY",
 }
 GEOM = {"cartesian": 0, "sine": 1}
-VARIANT = {"auto": 0, "general": 1, "tile": 2, "plane": 3, "halo": 6}
+VARIANT = {"auto": 0, "general": 1, "plane": 3, "halo": 6}
 
 
 class MFError(RuntimeError):

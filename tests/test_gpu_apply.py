@@ -89,14 +89,18 @@ TILE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("variant", ["general", "tile", "plane"])
+@pytest.mark.parametrize("variant", ["general", "plane", "halo"])
 @pytest.mark.parametrize("case", TILE_CASES, ids=_id)
 def test_cartesian_variants_match_oracle(case, variant, torch):
     p = oracle_problem(case)
     A = oracle.CSR(p)
     op = cuda_operator(case)
+    if variant == "halo" and not (case["k"] == 4 and (case["n_cells"][0] % 32 or case.get("dirichlet") is None
+                                                       or case["dirichlet"] & 2)
+                                  and (case["n_cells"][1] % 2 or case.get("dirichlet") is None or case["dirichlet"] & 8)):
+        pytest.skip("outside the halo kernel's domain (k = 4, Dirichlet x+ / y+ on full last tiles)")
     op.set_variant(variant)
-    assert op.info()["apply_variant"] == {"general": 1, "tile": 2, "plane": 3}[variant]
+    assert op.info()["apply_variant"] == {"general": 1, "plane": 3, "halo": 6}[variant]
     for s in (1, 2, 3):
         x = seeded(A.n, s)
         y_ref = A @ x
