@@ -279,7 +279,7 @@ mf_status mf_kernel_timing(mf_op *op, double *ms_total, int64_t *count);
 typedef struct mf_mg mf_mg; /* opaque */
 typedef struct {
   int32_t n_levels;        /* 0: halve while every direction is even and the coarser level has > max_coarse_dofs DoFs */
-  int64_t max_coarse_dofs; /* e.g. 1000; MF_ERR_ARGUMENT if the coarse level would exceed 8192 DoFs */
+  int64_t max_coarse_dofs; /* e.g. 1000; MF_ERR_ARGUMENT if the coarse level would exceed 2048 DoFs */
   int32_t smooth_degree;   /* Chebyshev degree of pre- and post-smoothing, 6 */
   double smooth_range;     /* 20 */
   double smooth_safety;    /* 1.2 */

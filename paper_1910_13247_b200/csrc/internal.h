@@ -169,6 +169,24 @@ mf_status hex_number_dofs(int k, int64_t n_cells, const int32_t *cell_vertices, 
 
 constexpr int kDotBlocks = 592;  // 4 x 148 SMs
 
+// Kernel attributes are per device: set them once per (kernel instance, device) -- ADVICE r01
+// (function-local statics had set them on the first device only)
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
+}
+template <class K>
+inline void smem_attr_once(K kernel, size_t bytes) {
+  static bool done[kMaxDevices] = {};  // one array per kernel instance
+  const int d = current_device();
+  if (!done[d]) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done[d] = true;
+  }
+}
+
 }  // namespace mf
 
 // api.cu internals shared with mg.cu (C++ linkage, not part of the C ABI)

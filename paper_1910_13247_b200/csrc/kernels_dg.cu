@@ -505,9 +505,7 @@ cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaS
     constexpr int CW = 2 * NV + 3, CT = 12 * NP;
     const int cpb = 256 / NP;
     const size_t smem = (size_t)(((cpb * CW + 1) & ~1) + cpb * CT + 2 * NP) * sizeof(double);
-    static bool attr2 = (cudaFuncSetAttribute(k_apply_dg2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                         true);
-    (void)attr2;
+    smem_attr_once(k_apply_dg2<K>, smem);
     const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
     (void)ncells;
     const int64_t blocks = (cend - cbeg + cpb - 1) / cpb;
@@ -519,9 +517,7 @@ cudaError_t launch_dg_t(const DGParams &D, const double *src, double *dst, cudaS
   while (cpb > 1 && (3 * cpb + 2) * NV * 8 > 96 * 1024) --cpb;
   if (cpb < 1) cpb = 1;
   const size_t smem = (size_t)(3 * cpb + 2) * NV * sizeof(double);  // own + x-neighbour cells, T, W
-  static bool attr = (cudaFuncSetAttribute(k_apply_dg<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
-                      true);
-  (void)attr;
+  smem_attr_once(k_apply_dg<K>, 96 * 1024);
   const int64_t ncells = D.nc[0] * D.nc[1] * D.nc[2];
   (void)ncells;
   const int64_t blocks = (cend - cbeg + cpb - 1) / cpb;

@@ -884,10 +884,7 @@ static cudaError_t launch_general_t(const Geo &g, const Tables &t, const double 
       constexpr int c3 = cell3_cpb<K, GEOM>();
       const int64_t b3 = (cend - cbeg + c3 - 1) / c3;
       const size_t sm3 = cell3_smem_bytes<K, GEOM, double>();
-      static bool attr = (cudaFuncSetAttribute(k_apply_cell3<K, GEOM, double>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3),
-                          true);
-      (void)attr;
+      smem_attr_once(k_apply_cell3<K, GEOM, double>, sm3);
       return launch_cell3_pdl<K, GEOM>((unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s, t, g, src, dst, metric, cbeg,
                                        cend, HexDev{});
     }
@@ -927,10 +924,7 @@ static cudaError_t launch_cell3_f32(const Geo &g, const TablesF &tf, const float
   const int64_t ncells = g.nc[0] * g.nc[1] * g.nc[2];
   const int64_t b3 = (ncells + c3 - 1) / c3;
   const size_t sm3 = cell3_smem_bytes<K, GEOM, float>();
-  static bool attr = (cudaFuncSetAttribute(k_apply_cell3<K, GEOM, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sm3),
-                      true);
-  (void)attr;
+  smem_attr_once(k_apply_cell3<K, GEOM, float>, sm3);
   if (b3 == 0) return cudaSuccess;
   k_apply_cell3<K, GEOM, float><<<(unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s>>>(tf, g, src, dst, metric, 0,
                                                                                       ncells, HexDev{});
@@ -1568,10 +1562,7 @@ static cudaError_t hex_apply_k(const Tables &t, const HexDev &h, const double *s
     constexpr int c3 = cell3_cpb<K, 3>();
     const int64_t b3 = (h.ncells + c3 - 1) / c3;
     const size_t sm3 = cell3_smem_bytes<K, 3, double>();
-    static bool attr = (cudaFuncSetAttribute(k_apply_cell3<K, 3, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sm3),
-                        true);
-    (void)attr;
+    smem_attr_once(k_apply_cell3<K, 3, double>, sm3);
     if (b3 == 0) return cudaSuccess;
     Geo g{};
     return launch_cell3_pdl<K, 3>((unsigned)b3, ((c3 * NP + 31) / 32) * 32, sm3, s, t, g, src, dst, h.metric, 0,

@@ -375,13 +375,13 @@ static cudaError_t launch_plane_t(const Geo &g, const Tables &t, const T *src, T
   using S = PlaneShape<K, TX, TY>;
   TileParams P;
   tile_params_common(g, t, TX, TY, &P);
-  static int occ = 0, sms = 0;
+  static int occ_d[kMaxDevices] = {}, sms_d[kMaxDevices] = {};  // per device
+  const int dev = current_device();
+  int &occ = occ_d[dev], &sms = sms_d[dev];
   if (occ == 0) {
     cudaFuncSetAttribute(k_apply_plane<K, TX, TY, ISO, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::template smem<T>());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_plane<K, TX, TY, ISO, T>, S::NT, S::template smem<T>());
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (occ < 1) occ = 1;
     if (sms < 1) sms = 148;
