@@ -92,6 +92,11 @@ bool cart_plane_supported(const Geo &g);
 cudaError_t launch_apply_cart_halo(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
                                    int64_t *launches, int part = 0, int zr_lo = 0, int zr_hi = 0);
 bool cart_halo_supported(const Geo &g);
+// kernels_tc.cu: Cartesian constant-coefficient 3D k = 5..7 on the FP64 tensor cores, the cell
+// layers [cz_lo, cz_hi) (scatter-add: dst zeroed by the caller; MF_NO_TC=1 disables it)
+cudaError_t launch_apply_tc(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,
+                            int cz_lo, int cz_hi);
+bool tc_supported(const Geo &g);
 // DG-SIP operator and its diagonal (kernels_dg.cu, §8(f) f4)
 // cells [cbeg, cend) only (cend < 0: every cell); DoFs cell-major, plain stores
 cudaError_t launch_apply_dg(const Geo &g, const Tables &t, const double *src, double *dst, cudaStream_t s,

@@ -988,7 +988,13 @@ static cudaError_t general_range(const Geo &g, const Tables &t, const double *sr
     if (gk == 1) return dispatch_k<2, 1>(g, t, src, dst, metric, s, cb, ce);
     return dispatch_k<2, 2>(g, t, src, dst, metric, s, cb, ce);
   }
-  if (gk == 0) return dispatch_k<3, 0>(g, t, src, dst, metric, s, cb, ce);
+  if (gk == 0) {
+    // k = 5..7: the DMMA kernel (kernels_tc.cu) over whole cell layers
+    const int64_t layer = g.nc[0] * g.nc[1];
+    if (tc_supported(g) && cb % layer == 0 && ce % layer == 0)
+      return launch_apply_tc(g, t, src, dst, s, (int)(cb / layer), (int)(ce / layer));
+    return dispatch_k<3, 0>(g, t, src, dst, metric, s, cb, ce);
+  }
   if (gk == 1) return dispatch_k<3, 1>(g, t, src, dst, metric, s, cb, ce);
   return dispatch_k<3, 2>(g, t, src, dst, metric, s, cb, ce);
 }
