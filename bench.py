@@ -73,6 +73,9 @@ def load_traffic(config):
 
 
 FP64_PEAK_TINSTR = 57.47 * 148 * 1.965e9 / 1e12  # measured DFMA issue rate (profiles/r01_microbench.json)
+# measured DMMA m8n8k4 f64 rate: 18.5 T FMA/s = 72.3 G DMMA/s, sharing the FP64 pipe additively
+# with DFMA (tools/micro/dmma_lat.cu, profiles/r02_dmma_microbench.txt)
+DMMA_PEAK_G = 18.5e12 / 256 / 1e9
 
 
 def fp64_roofline(config, n_dofs, kernel_ms):
@@ -80,12 +83,19 @@ def fp64_roofline(config, n_dofs, kernel_ms):
     (profiles/traffic.json) over the live kernel time, against the measured DFMA rate."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            ipd = json.load(f)[config]["fp64_instr_per_dof"]
+            e = json.load(f)[config]
+        ipd = e["fp64_instr_per_dof"]
     except Exception:
         return None
     achieved = ipd * n_dofs / (kernel_ms * 1e-3) / 1e12
-    return {"instr_per_dof": ipd, "achieved": achieved, "peak": FP64_PEAK_TINSTR, "unit": "T FP64 instr/s",
-            "frac": achieved / FP64_PEAK_TINSTR, "t_min_ms": ipd * n_dofs / (FP64_PEAK_TINSTR * 1e12) * 1e3}
+    t_min = ipd * n_dofs / (FP64_PEAK_TINSTR * 1e12) * 1e3
+    out = {"instr_per_dof": ipd, "achieved": achieved, "peak": FP64_PEAK_TINSTR, "unit": "T FP64 instr/s",
+           "frac": achieved / FP64_PEAK_TINSTR, "t_min_ms": t_min}
+    if e.get("dmma_per_dof"):  # tensor-core kernels: DMMA time on the same FP64 pipe
+        t_dmma = e["dmma_per_dof"] * n_dofs / (DMMA_PEAK_G * 1e9) * 1e3
+        out.update({"dmma_per_dof": e["dmma_per_dof"], "dmma_min_ms": t_dmma, "t_min_ms": t_min + t_dmma,
+                    "pipe_frac": (t_min + t_dmma) / kernel_ms})
+    return out
 
 
 def load_peaks():
@@ -182,14 +192,17 @@ def make_hex_operator(nc, k, coeff, device):
 
 def cpu_baseline_one_core(degree, geometry, coeff):
     """The same oracle SpMV on one host core (OMP_NUM_THREADS=1, fresh process), best of 5."""
+    # k >= 5: an 8^3 sub-brick (the 16^3 assembly alone is ~300 core-seconds for Q6)
+    cells = 8 if degree >= 5 else 16
     code = (f"import bench, json; v, nd, reps, el, ta, c = bench.cpu_baseline_sample({degree}, {geometry!r}, "
-            f"{coeff!r}, seconds=5.0); print(json.dumps([v, nd, c]))")
+            f"{coeff!r}, seconds=5.0, cells={cells}); print(json.dumps([v, nd, c]))")
     env = dict(os.environ, OMP_NUM_THREADS="1")
     try:
         r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True,
                            timeout=120)
         v, nd, c = json.loads(r.stdout.strip().splitlines()[-1])
-        return {"value": v, "unit": "DoFs/s", "cores": c, "sample": f"{nd} DoFs, best of 5 repeats of ~1 s"}
+        return {"value": v, "unit": "DoFs/s", "cores": c,
+                "sample": f"{cells}^3-cell sub-brick, {nd} DoFs, best of 5 repeats of ~1 s"}
     except Exception as e:  # the baseline is context; never fail the bench line on it
         return {"value": None, "error": str(e)[:200]}
 

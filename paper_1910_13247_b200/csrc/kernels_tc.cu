@@ -27,6 +27,11 @@
 //
 // Cost per cell (k = 6): 60 DMMA (16 SMSP cycles each) + ~136 DFMA-class lane instructions,
 // ~12 loads and ~12 reductions per lane, vs ~1870 warp instructions of the collocation form.
+// Registers bound the occupancy: the next cell's slices are prefetched one cell ahead (2 (N-1)
+// doubles), P and Q of every slice are held for the z step (4 N), and for k = 5, 6 the matrix
+// fragments are re-read from shared memory instead of being held (DESIGN.md §7.0b has the
+// variants measured).  Cells off the Dirichlet faces take a branch-free scatter; boundary
+// cells load their identity-row sources before storing (one latency instead of N).
 #include <cstdint>
 #include <cstdlib>
 
@@ -46,6 +51,12 @@ struct TcParams {
   int skip_top_identity;
 };
 
+#ifdef MF_TC_STORE  // timing experiment only: plain stores instead of reductions (wrong results)
+#define TC_RED(p, v) (*(p) = (v))
+#else
+#define TC_RED(p, v) atomicAdd((p), (v))
+#endif
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -53,7 +64,10 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 }
 
 // threads per block: 12 warps per SM for k = 5, 6 (<= 168 registers), 8 for k = 7 (~200)
-__host__ __device__ constexpr int tc_threads(int k) { return k == 7 ? 256 : 384; }
+#ifndef MF_TC_THREADS
+#define MF_TC_THREADS 384
+#endif
+__host__ __device__ constexpr int tc_threads(int k) { return k == 7 ? 256 : MF_TC_THREADS; }
 
 template <int K>
 __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_constant__ TcParams p,
@@ -62,6 +76,38 @@ __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_cons
   static_assert(N <= 8, "one 8x8 DMMA tile per slice");
   const int lane = threadIdx.x & 31, r = lane >> 2, c4 = lane & 3;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // the lane constants: fragment values of the 1D matrices, step-1 A operands (row y' = r,
+  // column y = 4 kk + c4) and step-2 B operands (B[k][n] = C[x' = r][x = 2 c4 + s] for k-step
+  // s).  For k = 5, 6 they live in shared memory and are re-read per use (volatile: not
+  // hoisted), so they do not hold 20 registers through the column walk (k = 6 then fits 12
+  // warps per SM without spilling); k = 7 runs 8 warps and keeps them in registers.
+  constexpr bool CSM = K != 7;
+  __shared__ double cst[CSM ? 10 : 1][32];
+  double creg[10];
+  auto fill = [&](double *c, int stride) {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      c[kk * stride] = p.M[r][4 * kk + c4];
+      c[(2 + kk) * stride] = p.fy * p.K[r][4 * kk + c4];
+      c[(4 + kk) * stride] = p.fx * p.K[r][2 * c4 + kk];
+      c[(6 + kk) * stride] = p.M[r][2 * c4 + kk];
+      c[(8 + kk) * stride] = p.fz * p.M[r][2 * c4 + kk];
+    }
+  };
+  if constexpr (CSM) {
+    if (threadIdx.x < 32) fill(&cst[0][lane], 32);
+    __syncthreads();
+  } else {
+    fill(creg, 1);
+  }
+  const volatile double *cs = &cst[0][lane];
+  auto C = [&](int i) -> double {
+    if constexpr (CSM) {
+      return cs[i * 32];
+    } else {
+      return creg[i];
+    }
+  };
   if (item >= p.items) return;
   const int cx = (int)(item % p.ncx);
   const int64_t t1 = item / p.ncx;
@@ -69,20 +115,6 @@ __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_cons
   const int c0 = p.cz_lo + chunk * p.lz, c1 = min(c0 + p.lz, p.cz_hi);
   const uint32_t d = p.dirichlet;
 
-  // lane constants: step-1 A operands (row y' = r, column y = 4 kk + c4), step-2 B operands
-  // (B[k][n] = C[x' = r][x = 2 c4 + s] for k-step s)
-  double Am[2], Ak[2], Bk[2], Bm[2], Bq[2];
-#pragma unroll
-  for (int kk = 0; kk < 2; ++kk) {
-    Am[kk] = p.M[r][4 * kk + c4];
-    Ak[kk] = p.fy * p.K[r][4 * kk + c4];
-  }
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    Bk[s] = p.fx * p.K[r][2 * c4 + s];
-    Bm[s] = p.M[r][2 * c4 + s];
-    Bq[s] = p.fz * p.M[r][2 * c4 + s];
-  }
   // the cell's x / y faces (fixed along the column)
   const bool fxm = (d & 1u) && cx == 0, fxp = (d & 2u) && cx == p.ncx - 1;
   const bool fym = (d & 4u) && cy == 0, fyp = (d & 8u) && cy == p.ncy - 1;
@@ -106,6 +138,7 @@ __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_cons
   }
   const int oofs = r * (int)p.Nx + 2 * c4;
   const int64_t colbase = (int64_t)K * cy * p.Nx + (int64_t)K * cx;
+  const bool xyface = fxm || fxp || fym || fyp;
 
   auto zcons = [&](int cz, int w) {
     return (w == 0 && (d & 16u) && cz == 0) || (w == N - 1 && (d & 32u) && cz == p.ncz - 1);
@@ -135,20 +168,20 @@ __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_cons
         continue;
       }
       double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-      dmma(a0, a1, Am[0], ub[w][0]);
-      dmma(b0, b1, Ak[0], ub[w][0]);
-      dmma(a0, a1, Am[1], ub[w][1]);
-      dmma(b0, b1, Ak[1], ub[w][1]);
+      dmma(a0, a1, C(0), ub[w][0]);
+      dmma(b0, b1, C(2), ub[w][0]);
+      dmma(a0, a1, C(1), ub[w][1]);
+      dmma(b0, b1, C(3), ub[w][1]);
       if (w >= 1 && !last) load_slice(cz + 1, w, ub[w]);  // next cell, one cell ahead
-      double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
-      dmma(p0, p1, a0, Bk[0]);
-      dmma(q0, q1, a0, Bq[0]);
-      dmma(p0, p1, a1, Bk[1]);
-      dmma(q0, q1, a1, Bq[1]);
-      dmma(p0, p1, b0, Bm[0]);
-      dmma(p0, p1, b1, Bm[1]);
-      P[w][0] = p0;
-      P[w][1] = p1;
+      double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0, r0 = 0.0, r1 = 0.0;
+      dmma(p0, p1, a0, C(4));
+      dmma(r0, r1, b0, C(6));
+      dmma(q0, q1, a0, C(8));
+      dmma(p0, p1, a1, C(5));
+      dmma(r0, r1, b1, C(7));
+      dmma(q0, q1, a1, C(9));
+      P[w][0] = p0 + r0;
+      P[w][1] = p1 + r1;
       Q[w][0] = q0;
       Q[w][1] = q1;
     }
@@ -190,13 +223,33 @@ __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_cons
         }
       }
       if (!ook[i]) continue;
+      if (!xyface && !zm && !zp) {  // no constrained node in this cell column
+        if (!first) v[0] += carry[i];
+#pragma unroll
+        for (int w = 0; w < N - 1; ++w) TC_RED(dst + cbase + (int64_t)w * p.plane + i, v[w]);
+        if (last) {
+          TC_RED(dst + cbase + (int64_t)(N - 1) * p.plane + i, v[N - 1]);
+        } else {
+          carry[i] = v[N - 1];
+        }
+        continue;
+      }
+      // identity rows: load every source value first (one latency, not N)
+      double idv[N];
+      bool idw[N];
+#pragma unroll
+      for (int w = 0; w < N; ++w) {
+        const int64_t gi = cbase + (int64_t)w * p.plane + i;
+        const bool cons = ocons[i] || (w == 0 && zm) || (w == N - 1 && zp);
+        idw[w] = cons && oown[i] && (w >= 1 || cz == 0) && !(w == N - 1 && skip);
+        idv[w] = idw[w] ? __ldg(src + gi) : 0.0;
+      }
 #pragma unroll
       for (int w = 0; w < N; ++w) {
         const int64_t gi = cbase + (int64_t)w * p.plane + i;
         const bool cons = ocons[i] || (w == 0 && zm) || (w == N - 1 && zp);
         if (cons) {
-          const bool owner = oown[i] && (w >= 1 || cz == 0) && !(w == N - 1 && skip);
-          if (owner) dst[gi] = __ldg(src + gi);
+          if (idw[w]) dst[gi] = idv[w];
           continue;
         }
         double val = v[w];
@@ -204,7 +257,7 @@ __global__ void __launch_bounds__(tc_threads(K), 1) k_apply_tc(const __grid_cons
         if (w == N - 1 && !last) {
           carry[i] = val;  // the top face: added by the cell above
         } else {
-          atomicAdd(dst + gi, val);
+          TC_RED(dst + gi, val);
         }
       }
     }
