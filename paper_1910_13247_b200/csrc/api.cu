@@ -909,18 +909,19 @@ static mf_status cheb_impl(mf_op *op, const double *r, double *x, double lam, in
   const double a = lam / range, b = lam;
   const double theta = 0.5 * (a + b), delta = 0.5 * (b - a), sigma = theta / delta;
   double rho = 1.0 / sigma;
-  CUDA_TRY(launch_cheb_init(r, op->dinv, 1.0 / theta, x, op->cd, n, op->stream, &op->launches));
+  // three-term form (kernels_vec.cu::k_cheb3): the iterates ping-pong between x and op->cd,
+  // the start x_1 = D^{-1} r / theta placed so that the last one lands in x
+  const int steps = degree - 1;
+  double *bx = (steps & 1) ? op->cd : x, *bp = (steps & 1) ? x : op->cd;
+  CUDA_TRY(launch_cheb_init1(r, op->dinv, 1.0 / theta, bx, n, op->stream, &op->launches));
   for (int j = 1; j < degree; ++j) {
     const double rho_n = 1.0 / (2.0 * sigma - rho);
-    STATUS_TRY(apply_impl(op, x, op->cax));
-    if (rz_dev && j == degree - 1) {
-      CUDA_TRY(launch_cheb_step_rz(r, op->cax, op->dinv, rho_n * rho, 2.0 * rho_n / delta, x, op->cd, n,
-                                   op->n_owned, op->partials, op->ticket, rz_dev, op->stream, &op->launches));
-      STATUS_TRY(allreduce_dev(op, rz_dev));
-      return MF_OK;
-    }
-    CUDA_TRY(launch_cheb_step(r, op->cax, op->dinv, rho_n * rho, 2.0 * rho_n / delta, x, op->cd, n, op->stream,
-                              &op->launches));
+    STATUS_TRY(apply_impl(op, bx, op->cax));
+    double *rz = (rz_dev && j == degree - 1) ? rz_dev : nullptr;  // r.z fused into the last step
+    CUDA_TRY(launch_cheb3(r, op->cax, op->dinv, rho_n * rho, 2.0 * rho_n / delta, bx, bp, j == 1, n, op->n_owned,
+                          op->partials, op->ticket, rz, op->stream, &op->launches));
+    if (rz) return allreduce_dev(op, rz_dev);
+    std::swap(bx, bp);
     rho = rho_n;
   }
   if (rz_dev) STATUS_TRY(dot_dev(op, r, x, rz_dev));

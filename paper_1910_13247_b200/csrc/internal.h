@@ -122,17 +122,16 @@ cudaError_t launch_cg_xr_rr(const double *rz, const double *pv, double *x, doubl
                             double *rr, cudaStream_t s, int64_t *launches);
 cudaError_t launch_cg_p_dev(const double *rz_new, const double *rz_old, const double *z, double *p, int64_t n,
                             cudaStream_t s, int64_t *launches);
-cudaError_t launch_cheb_step_rz(const double *r, const double *ax, const double *dinv, double c1, double c2,
-                                double *x, double *d, int64_t n, int64_t n_owned, double *partials,
-                                unsigned *ticket, double *rz, cudaStream_t s, int64_t *launches);
+// three-term Chebyshev step over x_{k-1} (xp; first: x_{k-1} = 0), optional fused r.x_{k+1}
+cudaError_t launch_cheb3(const double *r, const double *ax, const double *dinv, double c1, double c2,
+                         const double *x, double *xp, bool first, int64_t n, int64_t n_owned, double *partials,
+                         unsigned *ticket, double *rz, cudaStream_t s, int64_t *launches);
+cudaError_t launch_cheb_init1(const double *r, const double *dinv, double c0, double *x, int64_t n, cudaStream_t s,
+                              int64_t *launches);
 // y = a*x + b*y   (and variants used by CG / Chebyshev)
 cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t n, cudaStream_t s,
                          int64_t *launches);
-// Chebyshev: first step x = dinv*r*c0 (d = x), later d = c1*d + c2*dinv*(r - Ax); x += d
-cudaError_t launch_cheb_init(const double *r, const double *dinv, double c0, double *x, double *d, int64_t n,
-                             cudaStream_t s, int64_t *launches);
-cudaError_t launch_cheb_step(const double *r, const double *ax, const double *dinv, double c1, double c2,
-                             double *x, double *d, int64_t n, cudaStream_t s, int64_t *launches);
+// out = a * b elementwise (Jacobi), y = 1 / x
 cudaError_t launch_mul(const double *a, const double *b, double *out, int64_t n, cudaStream_t s,
                        int64_t *launches);
 cudaError_t launch_recip(const double *x, double *y, int64_t n, cudaStream_t s, int64_t *launches);

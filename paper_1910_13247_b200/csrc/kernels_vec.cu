@@ -156,33 +156,6 @@ cudaError_t launch_cg_p_dev(const double *rz_new, const double *rz_old, const do
   return cudaGetLastError();
 }
 
-// the last Chebyshev step with the CG's r.z fused: d = c1 d + c2 dinv (r - ax);
-// x += d; rz = r.x over the owned prefix
-__global__ void __launch_bounds__(256) k_cheb_step_rz(const double *__restrict__ r, const double *__restrict__ ax,
-                                                      const double *__restrict__ dinv, double c1, double c2,
-                                                      double *__restrict__ x, double *__restrict__ d, int64_t n,
-                                                      int64_t n_owned, double *partials, unsigned *ticket,
-                                                      double *rz) {
-  double acc[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double ri = r[i];
-    const double dn = c1 * d[i] + c2 * (dinv[i] * (ri - ax[i]));
-    d[i] = dn;
-    const double xn = x[i] + dn;
-    x[i] = xn;
-    if (i < n_owned) acc[0] = fma(ri, xn, acc[0]);
-  }
-  dot_finish<1>(acc, partials, ticket, rz);
-}
-
-cudaError_t launch_cheb_step_rz(const double *r, const double *ax, const double *dinv, double c1, double c2,
-                                double *x, double *d, int64_t n, int64_t n_owned, double *partials,
-                                unsigned *ticket, double *rz, cudaStream_t s, int64_t *launches) {
-  ++*launches;
-  k_cheb_step_rz<<<kDotBlocks, 256, 0, s>>>(r, ax, dinv, c1, c2, x, d, n, n_owned, partials, ticket, rz);
-  return cudaGetLastError();
-}
-
 __global__ void k_axpby(double a, const double *__restrict__ x, double b, double *__restrict__ y, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = a * x[i] + b * y[i];
@@ -195,37 +168,49 @@ cudaError_t launch_axpby(double a, const double *x, double b, double *y, int64_t
   return cudaGetLastError();
 }
 
-__global__ void k_cheb_init(const double *__restrict__ r, const double *__restrict__ dinv, double c0,
-                            double *__restrict__ x, double *__restrict__ d, int64_t n) {
+// three-term form of the same Chebyshev step (S:648-656 with d_{k-1} = x_k - x_{k-1}):
+// x_{k+1} = x_k + c1 (x_k - x_{k-1}) + c2 dinv (r - ax), written over x_{k-1} (xp; null: x_{k-1}
+// = 0, the first step from x_0 = 0); no separate direction vector, 48 instead of 56 bytes per
+// DoF.  With rz: r . x_{k+1} over the owned prefix (the CG's r.z, last step).
+template <bool RZ>
+__global__ void __launch_bounds__(256) k_cheb3(const double *__restrict__ r, const double *__restrict__ ax,
+                                               const double *__restrict__ dinv, double c1, double c2,
+                                               const double *__restrict__ x, double *xp, int64_t n, int64_t n_owned,
+                                               bool first, double *partials, unsigned *ticket, double *rz) {
+  double acc[1] = {0.0};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = r[i] * dinv[i] * c0;
-    x[i] = v;
-    d[i] = v;
+    const double ri = r[i], xi = x[i];
+    const double dk = first ? xi : xi - xp[i];
+    const double xn = xi + (c1 * dk + c2 * (dinv[i] * (ri - ax[i])));
+    xp[i] = xn;
+    if (RZ && i < n_owned) acc[0] = fma(ri, xn, acc[0]);
   }
+  if constexpr (RZ) dot_finish<1>(acc, partials, ticket, rz);
 }
 
-cudaError_t launch_cheb_init(const double *r, const double *dinv, double c0, double *x, double *d, int64_t n,
-                             cudaStream_t s, int64_t *launches) {
+cudaError_t launch_cheb3(const double *r, const double *ax, const double *dinv, double c1, double c2,
+                         const double *x, double *xp, bool first, int64_t n, int64_t n_owned, double *partials,
+                         unsigned *ticket, double *rz, cudaStream_t s, int64_t *launches) {
   ++*launches;
-  k_cheb_init<<<grid_for(n), 256, 0, s>>>(r, dinv, c0, x, d, n);
+  if (rz)
+    k_cheb3<true><<<kDotBlocks, 256, 0, s>>>(r, ax, dinv, c1, c2, x, xp, n, n_owned, first, partials, ticket, rz);
+  else
+    k_cheb3<false><<<grid_for(n), 256, 0, s>>>(r, ax, dinv, c1, c2, x, xp, n, n_owned, first, nullptr, nullptr,
+                                                nullptr);
   return cudaGetLastError();
 }
 
-// d = c1 d + c2 dinv (r - ax); x += d
-__global__ void k_cheb_step(const double *__restrict__ r, const double *__restrict__ ax,
-                            const double *__restrict__ dinv, double c1, double c2, double *__restrict__ x,
-                            double *__restrict__ d, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double dn = c1 * d[i] + c2 * (dinv[i] * (r[i] - ax[i]));
-    d[i] = dn;
-    x[i] += dn;
-  }
+// x = c0 dinv r (the Chebyshev start, x_0 = 0)
+__global__ void k_cheb_init1(const double *__restrict__ r, const double *__restrict__ dinv, double c0,
+                             double *__restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = r[i] * dinv[i] * c0;
 }
 
-cudaError_t launch_cheb_step(const double *r, const double *ax, const double *dinv, double c1, double c2,
-                             double *x, double *d, int64_t n, cudaStream_t s, int64_t *launches) {
+cudaError_t launch_cheb_init1(const double *r, const double *dinv, double c0, double *x, int64_t n, cudaStream_t s,
+                              int64_t *launches) {
   ++*launches;
-  k_cheb_step<<<grid_for(n), 256, 0, s>>>(r, ax, dinv, c1, c2, x, d, n);
+  k_cheb_init1<<<grid_for(n), 256, 0, s>>>(r, dinv, c0, x, n);
   return cudaGetLastError();
 }
 
