@@ -57,6 +57,27 @@ def test_chebyshev_matches_oracle(case, degree, torch):
     assert rel_l2(z, z_ref) <= 1e-12
 
 
+# more Chebyshev cases: anisotropic cells, Neumann and mixed faces, high degree (the k = 6 apply
+# runs on the DMMA kernel)
+MORE_CHEB_CASES = [
+    dict(dim=3, n_cells=(5, 3, 4), k=3, dirichlet=0b100110, upper=(1.0, 2.0, 0.5), coeff=3.0),
+    dict(dim=3, n_cells=(3, 2, 3), k=6, dirichlet=0b011001),
+    dict(dim=3, n_cells=(4, 3, 2), k=4, dirichlet=0, lower=(-0.5, 0.0, 0.2), upper=(1.0, 0.7, 1.0)),
+]
+
+
+@pytest.mark.parametrize("case", MORE_CHEB_CASES, ids=lambda c: f"k{c['k']}-d{c['dirichlet']}")
+@pytest.mark.parametrize("degree", [1, 6])
+def test_chebyshev_more_cases(case, degree, torch):
+    p, A, d, s = _oracle_setup(case)
+    op = cuda_operator(case)
+    r = synth.with_zero_dirichlet(seeded(A.n, 5), oracle.constrained_mask_fast(p))
+    lam = 1.2 * op.estimate_lambda_max(12)
+    z_ref = solvers.chebyshev(A.matvec, d, r, lam, degree, 20.0)
+    z = op.chebyshev(torch.from_numpy(r).cuda(), lam, degree, 20.0).cpu().numpy()
+    assert rel_l2(z, z_ref) <= 1e-12
+
+
 def _margin_ok(hist, tol, normb):
     if len(hist) < 2:
         return True
