@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/mf.h"
@@ -181,14 +183,23 @@ inline int current_device() {
   cudaGetDevice(&d);
   return d < 0 || d >= kMaxDevices ? 0 : d;
 }
+// keyed by (kernel address, device): a function-local static in a template over the kernel's
+// TYPE would be shared by every kernel of the same signature (k_apply_dg2<5> and <6>), and the
+// second one would launch without its attribute; a later larger request sets it again
+inline void smem_attr_once(const void *kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> set;
+  const int d = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &have = set[{kernel, d}];
+  if (have < bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    have = bytes;
+  }
+}
 template <class K>
 inline void smem_attr_once(K kernel, size_t bytes) {
-  static bool done[kMaxDevices] = {};  // one array per kernel instance
-  const int d = current_device();
-  if (!done[d]) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done[d] = true;
-  }
+  smem_attr_once(reinterpret_cast<const void *>(kernel), bytes);
 }
 
 }  // namespace mf
