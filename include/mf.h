@@ -74,10 +74,17 @@ typedef struct {
   double value;
 } mf_coeff;
 
-/* Multi-GPU placement; pass NULL to mf_create for one GPU on the current device. */
+/* Multi-GPU placement; pass NULL to mf_create for one GPU on the current device.
+ * world_size > 1 with nccl_unique_id == NULL builds a DETACHED slab operator: rank's z-slab
+ * exactly as in a distributed run (partition, interior z faces unconstrained, the upper rank
+ * writes the identity rows of a shared Dirichlet plane) but without a communicator.  mf_apply,
+ * mf_apply_split_part, mf_apply_host and mf_diagonal then return this rank's partial sums on
+ * the shared first / last plane; the caller adds the neighbour's (any transport).  Collective
+ * calls (dots, solvers, mf_chebyshev, lambda) fail with MF_ERR_ARGUMENT. */
 typedef struct {
   int32_t rank, world_size;
-  const uint8_t *nccl_unique_id; /* 128 bytes from mf_nccl_unique_id() on rank 0; NULL if world_size == 1 */
+  const uint8_t *nccl_unique_id; /* 128 bytes from mf_nccl_unique_id() on rank 0; NULL if world_size == 1
+                                    (or for a detached slab) */
   int32_t device;                /* CUDA device ordinal for this rank */
 } mf_dist;
 

@@ -43,6 +43,9 @@ struct mf_op {
   // halo overlap (§8(e)): the boundary cell layers first, the NCCL exchange of the shared
   // planes on comm_stream while the interior layers run on stream
   bool zsplit = false;  // world > 1, or MF_ZSPLIT=1 (the same launch sequence on one GPU)
+  // world > 1 without an NCCL unique id: the rank's slab operator with no communicator; the
+  // apply / diagonal return local partial sums on the shared planes, the caller exchanges them
+  bool detached = false;
   bool dg = false;      // discontinuous (SIP) discretization, mf_create_dg
   bool hex = false;     // unstructured hex mesh, mf_create_hex (device arrays in hx)
   HexDev hx{};
@@ -154,8 +157,7 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
     world = dist->world_size;
     device = dist->device;
     if (world < 1 || rank < 0 || rank >= world) return fail(MF_ERR_ARGUMENT, "bad rank/world_size");
-    if (world > 1 && (!dist->nccl_unique_id || mesh->dim != 3))
-      return fail(MF_ERR_ARGUMENT, "world_size > 1 needs dim 3 and an NCCL unique id");
+    if (world > 1 && mesh->dim != 3) return fail(MF_ERR_ARGUMENT, "world_size > 1 needs dim 3");
     if (world > 1 && mesh->n_cells[2] < world) return fail(MF_ERR_ARGUMENT, "fewer z cell layers than ranks");
   }
   if (device >= 0) CUDA_TRY(cudaSetDevice(device));
@@ -165,6 +167,7 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
   op->rank = rank;
   op->world = world;
   op->device = device;
+  op->detached = world > 1 && !dist->nccl_unique_id;
   Geo &g = op->g;
   std::memset(&g, 0, sizeof(Geo));
   g.dim = mesh->dim;
@@ -229,7 +232,7 @@ extern "C" mf_status mf_create(const mf_mesh *mesh, int32_t degree, const mf_coe
     if (e != cudaSuccess) return cleanup(fail(MF_ERR_CUDA, std::string("metric: ") + cudaGetErrorString(e)));
     if (hbad) return cleanup(fail(MF_ERR_SINGULAR, "det J <= 0 at a quadrature point"));
   }
-  if (world > 1) {
+  if (world > 1 && !op->detached) {
     ncclUniqueId id;
     std::memcpy(&id, dist->nccl_unique_id, 128);
     ncclResult_t nr = ncclCommInitRank(&op->comm, world, id, rank);
@@ -503,7 +506,7 @@ static mf_status halo_add(mf_op *op, double *dst) {
 }
 
 static mf_status halo_exchange(mf_op *op, double *dst) {
-  if (op->world == 1) return MF_OK;
+  if (op->world == 1 || op->detached) return MF_OK;
   STATUS_TRY(halo_post(op, dst, op->stream));
   return halo_add(op, dst);
 }
@@ -532,7 +535,7 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
     CUDA_TRY(launch_zero(dst, op->n_local, op->stream, &op->launches));
     CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches, 1));
   }
-  if (op->world > 1) {
+  if (op->world > 1 && !op->detached) {
     CUDA_TRY(cudaEventRecord(op->ev_bnd, op->stream));
     CUDA_TRY(cudaStreamWaitEvent(op->comm_stream, op->ev_bnd, 0));
     STATUS_TRY(halo_post(op, dst, op->comm_stream));
@@ -545,7 +548,7 @@ static mf_status apply_split(mf_op *op, const double *src, double *dst, int var)
   else
     CUDA_TRY(launch_apply_general(op->g, op->t, src, dst, op->metric, op->stream, &op->launches, 2));
   STATUS_TRY(timing_mark(op));
-  if (op->world > 1) {
+  if (op->world > 1 && !op->detached) {
     CUDA_TRY(cudaStreamWaitEvent(op->stream, op->ev_halo, 0));
     STATUS_TRY(halo_add(op, dst));
   }
@@ -749,6 +752,8 @@ extern "C" mf_status mf_diagonal(mf_op *op, double *diag, int64_t n) {
 }
 
 static mf_status ensure_solver(mf_op *op) {
+  // the solvers apply A repeatedly: a detached slab has no exchange, so they are refused
+  if (op->detached) return fail(MF_ERR_ARGUMENT, "detached slab operator: solvers need a communicator");
   if (op->r) return MF_OK;
   const size_t bytes = op->n_local * sizeof(double);
   for (double **b : {&op->diag, &op->dinv, &op->r, &op->p, &op->v, &op->z, &op->cd, &op->cax})
@@ -762,7 +767,7 @@ static mf_status ensure_solver(mf_op *op) {
 // ncclCommGetAsyncError != ncclSuccess, or no completion within MF_NCCL_TIMEOUT_S seconds
 // (a peer died or hung), aborts it and returns MF_ERR_NCCL (SURVEY §5 failure detection).
 static mf_status stream_wait(mf_op *op) {
-  if (op->world == 1) {
+  if (op->world == 1 || op->detached) {
     CUDA_TRY(cudaStreamSynchronize(op->stream));
     return MF_OK;
   }
@@ -797,6 +802,7 @@ extern "C" mf_status mf_sync(mf_op *op) {
 
 // nd dot products over the owned prefix, summed over ranks; result to host_scal[0..nd)
 static mf_status dots(mf_op *op, int nd, const double *const *a, const double *const *b) {
+  if (op->detached) return fail(MF_ERR_ARGUMENT, "detached slab operator: collective calls need a communicator");
   CUDA_TRY(launch_dots(nd, a, b, op->n_owned, op->partials, op->ticket, op->dev_scal, op->stream, &op->launches));
   if (op->world > 1) {
     if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
@@ -809,6 +815,7 @@ static mf_status dots(mf_op *op, int nd, const double *const *a, const double *c
 // a device scalar summed over the ranks, in stream order (no host synchronisation)
 static mf_status allreduce_dev(mf_op *op, double *x, int nd = 1) {
   if (op->world == 1) return MF_OK;
+  if (op->detached) return fail(MF_ERR_ARGUMENT, "detached slab operator: collective calls need a communicator");
   if (!op->comm) return fail(MF_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
   NCCL_TRY(ncclAllReduce(x, x, nd, ncclDouble, ncclSum, op->comm, op->stream));
   return MF_OK;

@@ -202,7 +202,7 @@ class Operator:
     [first_global, first_global + n_local) of the x-fastest global vector)."""
 
     def __init__(self, n_cells, degree, dim=None, lower=None, upper=None, geometry="cartesian", eps=0.1,
-                 coeff=1.0, dirichlet_faces=None, group=None, device=None, discretization="cg"):
+                 coeff=1.0, dirichlet_faces=None, group=None, device=None, discretization="cg", slab=None):
         import torch
 
         if not torch.cuda.is_available():
@@ -244,6 +244,8 @@ class Operator:
             self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
             dist.rank, dist.world_size = rank, world
             dist.nccl_unique_id = ctypes.cast(self._uid, ctypes.POINTER(ctypes.c_uint8))
+        elif slab is not None:  # detached slab (rank, world): partial sums on shared planes, no NCCL
+            dist.rank, dist.world_size = int(slab[0]), int(slab[1])
         else:
             dist.rank, dist.world_size = 0, 1
         with torch.cuda.device(device):
