@@ -68,6 +68,25 @@ def test_slab_decomposition_matches_oracle(cw, torch):
             np.testing.assert_array_equal(y[mask[sl]], x[sl][mask[sl]])
 
 
+@pytest.mark.parametrize("cw", [CASES[0], CASES[3], CASES[5], CASES[6]], ids=_id)
+def test_slab_diagonal_matches_oracle(cw, torch):
+    # mf_diagonal of a detached slab: partial sums on the shared planes, exchanged by the test
+    case, world = cw
+    p = oracle_problem(case)
+    d_ref = oracle.CSR(p).diagonal()
+    ops = [cuda_operator(case, slab=(r, world)) for r in range(world)]
+    plane = ops[0].n_local - ops[0].n_owned
+    part = [op.diagonal().cpu().numpy() for op in ops]
+    for r, op in enumerate(ops):
+        d = part[r].copy()
+        if r > 0:
+            d[:plane] += part[r - 1][-plane:]
+        if r < world - 1:
+            d[-plane:] += part[r + 1][:plane]
+        sl = slice(op.first_global, op.first_global + op.n_local)
+        assert rel_l2(d, d_ref[sl]) <= CUDA_ORACLE_TOL
+
+
 def test_slab_partition_matches_mf_partition(torch):
     from paper_1910_13247_b200.mf import partition
 

@@ -1,3 +1,3 @@
-# detached-slab decomposition parity + the apply suites that share its paths
+# detached-slab decomposition (apply, diagonal) + the >= 2-GPU NCCL test (skips on one GPU)
 set -x
-timeout 900 python -m pytest tests/test_gpu_slabs.py tests/test_gpu_halo.py tests/test_gpu_tc.py -x -q 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_slabs.py tests/test_gpu_multi.py -q -rs 2>&1 | tail -12
