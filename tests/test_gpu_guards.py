@@ -42,7 +42,9 @@ CASES = [
     (dict(dim=3, n_cells=(64, 4, 5), k=4), "auto"),              # halo, full last CTA (x+ column)
     (dict(dim=3, n_cells=(9, 10, 11), k=2), "plane"),
     (dict(dim=3, n_cells=(9, 9, 13), k=3), "plane"),
-    (dict(dim=3, n_cells=(4, 3, 5), k=6), "auto"),               # cell3 Cartesian Q6 (padded layout)
+    (dict(dim=3, n_cells=(4, 3, 5), k=6), "auto"),               # DMMA kernel (k_apply_tc), one chunk
+    (dict(dim=3, n_cells=(3, 2, 17), k=6, dirichlet=0), "auto"),  # DMMA kernel, z-chunks, Neumann
+    (dict(dim=3, n_cells=(2, 3, 9), k=7), "auto"),               # DMMA kernel, k = 7 (N = 8, no padding)
     (dict(dim=3, n_cells=(6, 5, 4), k=3, geometry="sine", coeff="variable"), "auto"),  # curved, TMA metric
     (dict(dim=2, n_cells=(7, 5), k=3), "auto"),
 ]
