@@ -99,6 +99,16 @@ def test_slab_partition_matches_mf_partition(torch):
                                                                   part["n_owned"])
 
 
+def test_slab_apply_host_equals_device_apply(torch):
+    # mf_apply_host on a slab (the non-pipelined host path, as the bench's e2e leg at N > 1)
+    case = dict(dim=3, n_cells=(5, 4, 8), k=4, dirichlet=0b011001)
+    for r in range(3):
+        op = cuda_operator(case, slab=(r, 3))
+        x = seeded(op.n_global, 4)[op.first_global:op.first_global + op.n_local].copy()
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        np.testing.assert_array_equal(op.apply_host(x), yd)
+
+
 def test_detached_slab_refuses_collectives(torch):
     from paper_1910_13247_b200 import MFError
 
