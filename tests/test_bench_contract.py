@@ -65,3 +65,29 @@ def test_reference_arm_world2_default_is_strong_scaling_cfg5():
     (d,) = _lines(r.stdout)
     assert d["scaling"] == "strong" and d["config"]["config"] == "cfg5q4"
     assert d["config"]["n_cells"] == [256, 256, 256] and d["config"]["n_dofs"] == 1025 ** 3
+
+
+@pytest.mark.gpu
+def test_main_arm_json_line_contract():
+    # the driver's bench contract on a small config: one JSON line with the keys it reads, the
+    # roofline / cpu_baseline / e2e / clocks objects, and a positive count of our own launches
+    env = dict(os.environ, OMP_NUM_THREADS="4")
+    r = subprocess.run([sys.executable, "bench.py", "--config", "cfg2", "--steps", "3", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _lines(r.stdout)
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["dtype"] == "f64" and d["value"] > 0 and d["gpu_launches"] > 0
+    ro = d["roofline"]
+    assert ro["bound"] in ("hbm", "tensor", "alu") and 0 < ro["frac"] < 1 and ro["unit"] == "GB/s"
+    assert abs(ro["frac"] - ro["achieved"] / ro["peak"]) < 1e-9
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["clocks"]["sm_max_mhz"] and "reasons" in d["clocks"]
+    assert d["identity_rows_exact"] is True
